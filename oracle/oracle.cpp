@@ -1,0 +1,805 @@
+// =============================================================================
+// ORACLE — plain, slow, single-threaded CPU reference for the ensemble solver.
+//
+// TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library. The product path
+// (paper_2304_06835_b200/) never imports, links or executes anything here, and
+// this file shares no code, header, table or constant with the CUDA path: every
+// coefficient below is typed in from the published method (citations inline).
+//
+// Citations: P:n = /root/reference/PAPER.md line n (arXiv 2304.06835);
+//            S:n = SPEC.md line n; "DESIGN R<k>" = reading k in DESIGN.md §3.
+//
+// Build (by build.py): g++ -O2 -std=c++17 -ffp-contract=off -fno-fast-math
+//   -shared -fPIC. No contraction: every fused multiply-add is an explicit
+//   std::fma and appears exactly where DESIGN.md §4 (canonical operation order)
+//   puts one; every other operation is a separately rounded IEEE op in T.
+//
+// Pins (tests/test_oracle_*.py, -m "not gpu"): tableau order conditions,
+// stability-polynomial closed forms, convergence orders, Robertson literature
+// values and mass conservation, Philox known-answer vectors, exact discrete
+// EM moments for GBM, LU vs Cramer, model values/Jacobians vs finite
+// differences, stats on exact small cases.
+// Parity unpinned (oracle-vs-GPU only): the PI-controller
+// constants (R2) and the stochastic-Lorenz diffusion (R9) — the paper does not
+// print them.
+// =============================================================================
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include <limits>
+
+namespace orc {
+
+// ---------------------------------------------------------------- enums ----
+// Numbering mirrors include/ens.h (an interface fact, not shared code).
+enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
+             GBM = 4, EXPDECAY = 5, HARMONIC = 6 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2 };
+enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
+
+struct Dims { int n, m, nw; bool sde; };
+static bool dims(int model, Dims* d) {
+  switch (model) {
+    case LORENZ:         *d = {3, 3, 0, false}; return true;
+    case ROBERTSON:      *d = {3, 3, 0, false}; return true;
+    case LORENZ_SDE_ADD: *d = {3, 4, 3, true};  return true;   // DESIGN R9
+    case LORENZ_SDE_MUL: *d = {3, 4, 3, true};  return true;   // DESIGN R9
+    case GBM:            *d = {3, 2, 3, true};  return true;
+    case EXPDECAY:       *d = {1, 1, 0, false}; return true;   // test model (closed form)
+    case HARMONIC:       *d = {2, 1, 0, false}; return true;   // test model (closed form)
+  }
+  return false;
+}
+
+// --------------------------------------------------------------- models ----
+// Right-hand sides f(u,p,t), written in the canonical order of
+// DESIGN.md §4 so that the oracle and the kernel round identically.
+template <class T>
+static void rhs(int model, const T* y, const T* p, T /*t*/, T* f) {
+  switch (model) {
+    case LORENZ: case LORENZ_SDE_ADD: case LORENZ_SDE_MUL: {
+      // dy1 = σ(y2 − y1); dy2 = ρ y1 − y2 − y1 y3; dy3 = y1 y2 − γ y3
+      const T sigma = p[0], rho = p[1], beta = p[2];
+      f[0] = sigma * (y[1] - y[0]);
+      f[1] = std::fma(y[0], rho - y[2], -y[1]);
+      f[2] = std::fma(y[0], y[1], -(beta * y[2]));
+      return;
+    }
+    case ROBERTSON: {
+      // P:671-677 with (k1,k2,k3) = (p0,p1,p2) = (0.04, 3e7, 1e4):
+      // dy1 = −k1 y1 + k3 y2 y3; dy2 = k1 y1 − k3 y2 y3 − k2 y2²; dy3 = k2 y2²
+      const T k1 = p[0], k2 = p[1], k3 = p[2];
+      const T k3y2y3 = (k3 * y[1]) * y[2];
+      f[0] = std::fma(-k1, y[0], k3y2y3);
+      f[2] = (k2 * y[1]) * y[1];
+      f[1] = std::fma(k1, y[0], -k3y2y3) - f[2];
+      return;
+    }
+    case GBM: {
+      // dX = r X dt + V X dW (drift part)
+      const T r = p[0];
+      for (int j = 0; j < 3; ++j) f[j] = r * y[j];
+      return;
+    }
+    case EXPDECAY: f[0] = (-p[0]) * y[0]; return;          // u' = −λu
+    case HARMONIC: f[0] = y[1]; f[1] = -(p[0] * y[0]); return;  // x' = v, v' = −ω² x
+  }
+}
+
+// Diagonal diffusion b(u,p,t) for SDE models.
+template <class T>
+static void diffusion(int model, const T* y, const T* p, T /*t*/, T* b) {
+  switch (model) {
+    case LORENZ_SDE_ADD: for (int j = 0; j < 3; ++j) b[j] = p[3]; return;          // R9: b_j = s
+    case LORENZ_SDE_MUL: for (int j = 0; j < 3; ++j) b[j] = p[3] * y[j]; return;   // R9: b_j = s u_j
+    case GBM:            for (int j = 0; j < 3; ++j) b[j] = p[1] * y[j]; return;   // V X
+  }
+}
+
+// Analytic Jacobian ∂f/∂u (row-major J[i*n+j] = ∂f_i/∂u_j). The paper uses
+// in-kernel forward-mode AD; the oracle uses the hand-derived exact
+// Jacobian of the same f (pinned against central differences in the tests).
+template <class T>
+static void jac(int model, const T* y, const T* p, T /*t*/, T* J) {
+  switch (model) {
+    case LORENZ: case LORENZ_SDE_ADD: case LORENZ_SDE_MUL: {
+      const T sigma = p[0], rho = p[1], beta = p[2];
+      J[0] = -sigma;      J[1] = sigma; J[2] = T(0);
+      J[3] = rho - y[2];  J[4] = T(-1); J[5] = -y[0];
+      J[6] = y[1];        J[7] = y[0];  J[8] = -beta;
+      return;
+    }
+    case ROBERTSON: {
+      const T k1 = p[0], k2 = p[1], k3 = p[2];
+      const T a = k3 * y[2], b = k3 * y[1], c = (k2 * y[1]) * T(2);
+      J[0] = -k1; J[1] = a;          J[2] = b;
+      J[3] = k1;  J[4] = (-a) - c;   J[5] = -b;
+      J[6] = T(0); J[7] = c;         J[8] = T(0);
+      return;
+    }
+    case EXPDECAY: J[0] = -p[0]; return;
+    case HARMONIC: J[0] = T(0); J[1] = T(1); J[2] = -p[0]; J[3] = T(0); return;
+  }
+}
+
+// ------------------------------------------------------- Tsit5 tableau ----
+// Tsitouras 2011 5(4) pair, cited by the paper as GPUTsit5. Values as
+// published (SURVEY.md App. A reproduces them); stored as double literals and
+// converted to T exactly once (DESIGN R7).
+static const double TS_C[7] = {0.0, 0.161, 0.327, 0.9, 0.9800255409045097, 1.0, 1.0};
+static const double TS_A[7][7] = {
+  {0, 0, 0, 0, 0, 0, 0},
+  {0.161, 0, 0, 0, 0, 0, 0},
+  {-0.008480655492356989, 0.335480655492357, 0, 0, 0, 0, 0},
+  {2.897153057105493, -6.359448489975075, 4.3622954328695815, 0, 0, 0, 0},
+  {5.325864828439257, -11.748883564062828, 7.4955393428898365, -0.09249506636175525, 0, 0, 0},
+  {5.86145544294642, -12.92096931784711, 8.159367898576159, -0.071584973281401, -0.028269050394068383, 0, 0},
+  {0.09646076681806523, 0.01, 0.4798896504144996, 1.379008574103742, -3.290069515436081, 2.324710524099774, 0}};
+// b = row 7 of A (FSAL), b7 = 0.
+// b̃ = b − b̂ (the embedded 4th-order weights enter only through b̃).
+static const double TS_BTILDE[7] = {-0.00178001105222577714, -0.0008164344596567469, 0.007880878010261995,
+                                    -0.1447110071732629, 0.5823571654525552, -0.45808210592918697,
+                                    0.015151515151515152};
+// Free 4th-order dense output ("free 4th-order interpolation"):
+// b_1(θ) = θ(r11 + θ(r12 + θ(r13 + θ r14))), b_i(θ) = θ²(r_i2 + θ(r_i3 + θ r_i4)).
+static const double TS_R[7][4] = {
+  {1.0, -2.763706197274826, 2.9132554618219126, -1.0530884977290216},
+  {0.0, 0.13169999999999998, -0.2234, 0.1017},
+  {0.0, 3.9302962368947516, -5.941033872131505, 2.490627285651253},
+  {0.0, -12.411077166933676, 30.33818863028232, -16.548102889244902},
+  {0.0, 37.50931341651104, -88.1789048947664, 47.37952196281928},
+  {0.0, -27.896526289197286, 65.09189467479366, -34.87065786149661},
+  {0.0, 1.5, -4.0, 2.5}};
+
+// PI step-size controller: h_new = η q_{n-1}^{β2} q_n^{-β1} h — signs,
+// η, β and clamps are DESIGN R2 (the paper prints none of them).
+struct Ctrl { double beta1, beta2, eta, qmin_inv, qmax_inv, qold_floor; };
+static const Ctrl CTRL_TSIT5 = {7.0 / 50.0, 2.0 / 25.0, 0.9, 5.0, 0.1, 1e-4};   // p=5: 7/(10p), 2/(5p)
+static const Ctrl CTRL_ROS23 = {7.0 / 20.0, 2.0 / 10.0, 0.9, 5.0, 0.1, 1e-4};   // p=2
+
+// ------------------------------------------------ Rosenbrock23 constants ----
+// ode23s pair of Shampine & Reichelt (cited for Rosenbrock23).
+static const double R23_D = 0.29289321881345248;   // d = 1/(2+√2)
+static const double R23_E32 = 7.414213562373095;   // e32 = 6+√2
+
+// ---------------------------------------------------------------- Philox ----
+// Philox4x32-10 (Salmon et al. 2011), the counter-based generator chosen for
+// the paper's per-trajectory seeded SDE noise (DESIGN R8).
+static void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    if (round < 9) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+  }
+  for (int i = 0; i < 4; ++i) out[i] = c[i];
+}
+
+// Uniforms in the open interval (0,1), exact in T (DESIGN R8).
+static float u01_f32(uint32_t w) { return ((float)(w >> 9) + 0.5f) * 1.1920928955078125e-07f; }  // 2^-23
+static double u01_f64(uint32_t wa, uint32_t wb) {
+  const double x = (double)wa * 1048576.0 + (double)(wb >> 12);   // 52-bit integer
+  return (x + 0.5) * 2.220446049250313080847263336181640625e-16;  // 2^-52
+}
+
+// cospi / sinpi of x ∈ [0,2): reduced exactly to a quarter period, then
+// evaluated with the C library's cos/sin of π·r in long double (≤1 ulp in T).
+template <class T> static void sincospi_ref(T x, T* s, T* c) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double a = pi * (long double)x;
+  *s = (T)std::sin(a);
+  *c = (T)std::cos(a);
+}
+
+// Three standard normals for (trajectory gidx, step i): Box–Muller on Philox
+// uniforms; counter = (step, gidx lo, gidx hi, call), key = (seed lo, seed hi)
+// (DESIGN R8). fp32: one call, pairs (U0,U1),(U2,U3); fp64: two calls, each
+// pair (U_a,U_b) from one call. Fourth normal dropped.
+template <class T> static void normals3(uint64_t seed, uint64_t step, uint64_t gidx, T z[3]);
+template <> void normals3<float>(uint64_t seed, uint64_t step, uint64_t gidx, float z[3]) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), 0u};
+  uint32_t w[4]; philox4x32_10(ctr, key, w);
+  float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
+  float s, c;
+  float R = std::sqrt(-2.0f * std::log(U[0]));
+  sincospi_ref<float>(2.0f * U[1], &s, &c);
+  z[0] = R * c; z[1] = R * s;
+  R = std::sqrt(-2.0f * std::log(U[2]));
+  sincospi_ref<float>(2.0f * U[3], &s, &c);
+  z[2] = R * c;
+}
+template <> void normals3<double>(uint64_t seed, uint64_t step, uint64_t gidx, double z[3]) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  double U[4];
+  for (uint32_t call = 0; call < 2; ++call) {
+    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), call};
+    uint32_t w[4]; philox4x32_10(ctr, key, w);
+    U[2 * call] = u01_f64(w[0], w[1]);
+    U[2 * call + 1] = u01_f64(w[2], w[3]);
+  }
+  double s, c;
+  double R = std::sqrt(-2.0 * std::log(U[0]));
+  sincospi_ref<double>(2.0 * U[1], &s, &c);
+  z[0] = R * c; z[1] = R * s;
+  R = std::sqrt(-2.0 * std::log(U[2]));
+  sincospi_ref<double>(2.0 * U[3], &s, &c);
+  z[2] = R * c;
+}
+
+// ------------------------------------------------------ fixed-step grid ----
+// DESIGN R3: number of fixed steps and the last step, computed in fp64.
+static void fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last) {
+  const double r = (tf - t0) / dt;
+  const double rr = std::nearbyint(r);
+  int64_t ns = (std::fabs(r - rr) <= 1e-9 * std::max(1.0, r)) ? (int64_t)rr : (int64_t)std::ceil(r);
+  if (ns < 1) ns = 1;
+  *nsteps = ns;
+  *h_last = (tf - t0) - (double)(ns - 1) * dt;
+}
+
+template <class T> static bool finite_vec(const T* v, int n) {
+  for (int j = 0; j < n; ++j) if (!std::isfinite(v[j])) return false;
+  return true;
+}
+
+// Per-trajectory problem + outputs (one column of the paper's U / P).
+template <class T> struct Traj {
+  int n, m;
+  T u0[8], p[8];
+  uint64_t gidx;                 // global trajectory index (Philox counter)
+  // outputs
+  T* save;                       // [k][n] row-major for this trajectory (k = nsave) or [n] final
+  int32_t retcode, n_accept, n_reject;
+};
+
+struct Opts {
+  int model, alg, adaptive;
+  double t0, tf, dt, abstol, reltol;
+  int64_t max_steps;
+  uint64_t seed;
+  const double* saveat; int k;
+};
+
+// ---------------------------------------------------------------- Tsit5 ----
+// One Tsit5 step from (t,u,k1) with step h:
+//   y_i = u + h Σ_{j<i} a_ij k_j,  k_i = f(y_i, t + c_i h)   (i = 2..7)
+//   u_{n+1} = y_7 (FSAL: b = a_7·), k7 = f(u_{n+1}) = next k1
+//   E = h Σ b̃_i k_i (b̃ = b − b̂)
+// Canonical order: acc = a_i1 k1; acc = fma(a_ij, k_j, acc);
+// y = fma(h, acc, u).
+template <class T>
+static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7][8], T* unew, T* E) {
+  T y[8];
+  for (int i = 1; i < 7; ++i) {
+    for (int j = 0; j < n; ++j) {
+      T acc = (T)TS_A[i][0] * K[0][j];
+      for (int l = 1; l < i; ++l) acc = std::fma((T)TS_A[i][l], K[l][j], acc);
+      y[j] = std::fma(h, acc, u[j]);
+    }
+    const T ti = t + (T)TS_C[i] * h;
+    rhs<T>(model, y, p, ti, K[i]);
+  }
+  for (int j = 0; j < n; ++j) unew[j] = y[j];
+  if (E) {
+    for (int j = 0; j < n; ++j) {
+      T e = (T)TS_BTILDE[0] * K[0][j];
+      for (int l = 1; l < 7; ++l) e = std::fma((T)TS_BTILDE[l], K[l][j], e);
+      E[j] = h * e;
+    }
+  }
+}
+
+// Tsit5 free interpolant at θ ∈ (0,1) (DESIGN §4 order).
+template <class T>
+static void tsit5_interp(int n, T theta, T h, const T* u, T K[7][8], T* out) {
+  T bt[7];
+  bt[0] = std::fma(theta, std::fma(theta, std::fma(theta, (T)TS_R[0][3], (T)TS_R[0][2]), (T)TS_R[0][1]),
+                   (T)TS_R[0][0]) * theta;
+  const T th2 = theta * theta;
+  for (int i = 1; i < 7; ++i)
+    bt[i] = std::fma(theta, std::fma(theta, (T)TS_R[i][3], (T)TS_R[i][2]), (T)TS_R[i][1]) * th2;
+  for (int j = 0; j < n; ++j) {
+    T acc = bt[0] * K[0][j];
+    for (int i = 1; i < 7; ++i) acc = std::fma(bt[i], K[i][j], acc);
+    out[j] = std::fma(h, acc, u[j]);
+  }
+}
+
+// Error proportion q (P:117-119 Eq. q), RMS norm (DESIGN R4), component-wise max.
+template <class T>
+static T error_q(int n, const T* E, const T* u, const T* unew, T abstol, T reltol) {
+  T s = T(0);
+  for (int j = 0; j < n; ++j) {
+    const T sc = abstol + reltol * std::fmax(std::fabs(u[j]), std::fabs(unew[j]));
+    const T r = E[j] / sc;
+    s = (j == 0) ? r * r : std::fma(r, r, s);
+  }
+  T q = std::sqrt(s / (T)n);
+  if (!std::isfinite(q)) q = std::numeric_limits<T>::infinity();
+  return q;
+}
+
+// Store helpers: save buffer is [k][n] for one trajectory.
+template <class T> static void put(T* save, int n, int j, const T* v) {
+  for (int c = 0; c < n; ++c) save[j * n + c] = v[c];
+}
+
+// PI controller (DESIGN R2). Returns the new h after an accepted step.
+template <class T> static T pi_accept(const Ctrl& C, T h, T q, T* q_old) {
+  const T q11 = std::pow(q, (T)C.beta1);
+  T qq = q11 / std::pow(*q_old, (T)C.beta2);
+  qq = std::fmax((T)C.qmax_inv, std::fmin((T)C.qmin_inv, qq / (T)C.eta));
+  *q_old = std::fmax(q, (T)C.qold_floor);
+  return h / qq;
+}
+template <class T> static T pi_reject(const Ctrl& C, T h, T q) {
+  return h / std::fmin((T)C.qmin_inv, std::pow(q, (T)C.beta1) / (T)C.eta);
+}
+
+template <class T>
+static void solve_tsit5(const Opts& o, Traj<T>& tr) {
+  const int n = tr.n, model = o.model;
+  T u[8], K[7][8], unew[8], E[8];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  const int k = o.k;
+  std::vector<T> tau(k);
+  for (int j = 0; j < k; ++j) tau[j] = (T)o.saveat[j];
+  int js = 0;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  T t = (T)o.t0;
+  const T tf = (T)o.tf;
+  rhs<T>(model, u, p, t, K[0]);
+  // saves at τ_j == t0 (DESIGN R5)
+  while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; }
+  if (!finite_vec(K[0], n)) { tr.retcode = RET_DIVERGED; }
+  else if (!o.adaptive) {
+    // Fixed step (DESIGN R3): t_i = t0 + i dt in fp64, h = dt except the last.
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    const T hdt = (T)o.dt, hl = (T)h_last;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const bool last = (i == nsteps - 1);
+      const T h = last ? hl : hdt;
+      t = (T)(o.t0 + (double)i * o.dt);
+      tsit5_step<T>(model, n, p, t, h, u, K, unew, nullptr);
+      const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
+      while (js < k && tau[js] <= tn) {
+        if (tau[js] == tn) put(tr.save, n, js, unew);
+        else { T out[8]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
+        ++js;
+      }
+      for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
+      tr.n_accept++;
+    }
+    t = tf;
+    if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;   // DESIGN R6
+  } else {
+    // Adaptive (DESIGN R2, R5).
+    const Ctrl& C = CTRL_TSIT5;
+    const T abstol = (T)o.abstol, reltol = (T)o.reltol;
+    T h = (T)std::min(o.dt, o.tf - o.t0);
+    T q_old = (T)C.qold_floor;
+    int64_t attempts = 0;
+    while (t < tf) {
+      if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
+      const bool last = (t + h >= tf);
+      if (last) h = tf - t;
+      tsit5_step<T>(model, n, p, t, h, u, K, unew, E);
+      const T q = error_q<T>(n, E, u, unew, abstol, reltol);
+      ++attempts;
+      if (q < T(1)) {                              // accept iff q < 1
+        const T tn = last ? tf : t + h;
+        while (js < k && tau[js] <= tn) {
+          if (tau[js] == tn) put(tr.save, n, js, unew);
+          else { T out[8]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
+          ++js;
+        }
+        t = tn;
+        for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
+        tr.n_accept++;
+        h = pi_accept<T>(C, h, q, &q_old);
+      } else {
+        h = pi_reject<T>(C, h, q);
+        tr.n_reject++;
+      }
+      if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
+    }
+  }
+  if (k == 0) put(tr.save, n, 0, u);
+  else {
+    const T nan = std::numeric_limits<T>::quiet_NaN();
+    T nv[8]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    for (; js < k; ++js) put(tr.save, n, js, nv);   // unreached save points (DESIGN R6)
+  }
+}
+
+// --------------------------------------------------------- Rosenbrock23 ----
+// Dense LU with partial pivoting ("LU factorization … forward and
+// backward substitution"), canonical order of DESIGN §4. A is row-major n×n,
+// overwritten by L (unit, strictly lower) and U; piv[k] = pivot row at step k;
+// inv[i] = 1/U_ii. Returns false if a pivot is exactly zero or non-finite.
+template <class T>
+static bool lu_factor(int n, T* A, int* piv, T* inv) {
+  for (int kk = 0; kk < n; ++kk) {
+    int pr = kk; T best = std::fabs(A[kk * n + kk]);
+    for (int i = kk + 1; i < n; ++i) {
+      const T v = std::fabs(A[i * n + kk]);
+      if (v > best) { best = v; pr = i; }
+    }
+    piv[kk] = pr;
+    if (pr != kk) for (int j = 0; j < n; ++j) std::swap(A[kk * n + j], A[pr * n + j]);
+    const T pivot = A[kk * n + kk];
+    if (pivot == T(0) || !std::isfinite(pivot)) return false;
+    inv[kk] = T(1) / pivot;
+    for (int i = kk + 1; i < n; ++i) {
+      const T l = A[i * n + kk] * inv[kk];
+      A[i * n + kk] = l;
+      for (int j = kk + 1; j < n; ++j) A[i * n + j] = std::fma(-l, A[kk * n + j], A[i * n + j]);
+    }
+  }
+  return true;
+}
+template <class T>
+static void lu_solve(int n, const T* LU, const int* piv, const T* inv, const T* b, T* x) {
+  T z[8];
+  for (int i = 0; i < n; ++i) z[i] = b[i];
+  for (int kk = 0; kk < n; ++kk) if (piv[kk] != kk) std::swap(z[kk], z[piv[kk]]);
+  for (int i = 0; i < n; ++i) {            // forward: unit lower
+    T s = z[i];
+    for (int j = 0; j < i; ++j) s = std::fma(-LU[i * n + j], z[j], s);
+    z[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {       // backward
+    T s = z[i];
+    for (int j = i + 1; j < n; ++j) s = std::fma(-LU[i * n + j], x[j], s);
+    x[i] = s * inv[i];
+  }
+}
+
+// One ode23s step (DESIGN R10; P:124-138 general form with the Shampine &
+// Reichelt coefficients). F0 = f(u,t) is FSAL. Autonomous models: ∂f/∂t = 0.
+// Returns false if W is singular.
+template <class T>
+static bool ros23_step(int model, int n, const T* p, T t, T h, const T* u, const T* F0,
+                       T* unew, T* F2, T* k1, T* k2, T* E) {
+  const T d = (T)R23_D, e32 = (T)R23_E32;
+  T J[64], W[64], inv[8]; int piv[8];
+  jac<T>(model, u, p, t, J);
+  const T hd = h * d;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) W[i * n + j] = (i == j ? T(1) : T(0)) - hd * J[i * n + j];  // W = I − h d J
+  if (!lu_factor<T>(n, W, piv, inv)) return false;
+  T rhsv[8], y[8], F1[8], k3[8];
+  lu_solve<T>(n, W, piv, inv, F0, k1);                                  // k1 = W⁻¹ F0
+  const T hh = h * T(0.5);
+  for (int j = 0; j < n; ++j) y[j] = std::fma(hh, k1[j], u[j]);        // u + h/2 k1
+  rhs<T>(model, y, p, t + hh, F1);                                      // F1
+  for (int j = 0; j < n; ++j) rhsv[j] = F1[j] - k1[j];
+  lu_solve<T>(n, W, piv, inv, rhsv, k2);
+  for (int j = 0; j < n; ++j) k2[j] = k2[j] + k1[j];                    // k2 = W⁻¹(F1 − k1) + k1
+  for (int j = 0; j < n; ++j) unew[j] = std::fma(h, k2[j], u[j]);      // u_new = u + h k2
+  rhs<T>(model, unew, p, t + h, F2);                                    // F2
+  for (int j = 0; j < n; ++j) {                                         // F2 − e32(k2 − F1) − 2(k1 − F0)
+    const T a = std::fma(-e32, k2[j] - F1[j], F2[j]);
+    rhsv[j] = std::fma(T(-2), k1[j] - F0[j], a);
+  }
+  lu_solve<T>(n, W, piv, inv, rhsv, k3);                                // k3
+  const T h6 = h / T(6);
+  for (int j = 0; j < n; ++j) {                                         // E = h/6 (k1 − 2 k2 + k3)
+    const T s = std::fma(T(-2), k2[j], k1[j]) + k3[j];
+    E[j] = h6 * s;
+  }
+  return true;
+}
+
+// ode23s continuous extension ("second-order stiff-aware interpolation"):
+// u(t+θh) = u + h[θ(1−θ)/(1−2d) k1 + θ(θ−2d)/(1−2d) k2].
+template <class T>
+static void ros23_interp(int n, T theta, T h, const T* u, const T* k1, const T* k2, T* out) {
+  const T d = (T)R23_D;
+  const T inv12d = (T)(1.0 / (1.0 - 2.0 * R23_D));
+  const T c1 = (theta * (T(1) - theta)) * inv12d;
+  const T c2 = (theta * (theta - T(2) * d)) * inv12d;
+  for (int j = 0; j < n; ++j) {
+    const T acc = std::fma(c2, k2[j], c1 * k1[j]);
+    out[j] = std::fma(h, acc, u[j]);
+  }
+}
+
+template <class T>
+static void solve_ros23(const Opts& o, Traj<T>& tr) {
+  const int n = tr.n, model = o.model;
+  const Ctrl& C = CTRL_ROS23;
+  T u[8], F0[8], unew[8], F2[8], k1[8], k2[8], E[8];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  const int k = o.k;
+  std::vector<T> tau(k);
+  for (int j = 0; j < k; ++j) tau[j] = (T)o.saveat[j];
+  int js = 0;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  T t = (T)o.t0;
+  const T tf = (T)o.tf, abstol = (T)o.abstol, reltol = (T)o.reltol;
+  rhs<T>(model, u, p, t, F0);
+  while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; }
+  if (!finite_vec(F0, n)) tr.retcode = RET_DIVERGED;
+  else if (!o.adaptive) {
+    // Fixed step (DESIGN R3): same grid rule as Tsit5; a singular W ends the
+    // trajectory with RET_SINGULAR (no step-size fallback without control).
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    const T hdt = (T)o.dt, hl = (T)h_last;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const bool last = (i == nsteps - 1);
+      const T h = last ? hl : hdt;
+      t = (T)(o.t0 + (double)i * o.dt);
+      if (!ros23_step<T>(model, n, p, t, h, u, F0, unew, F2, k1, k2, E)) { tr.retcode = RET_SINGULAR; break; }
+      const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
+      while (js < k && tau[js] <= tn) {
+        if (tau[js] == tn) put(tr.save, n, js, unew);
+        else { T out[8]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
+        ++js;
+      }
+      for (int j = 0; j < n; ++j) { u[j] = unew[j]; F0[j] = F2[j]; }
+      tr.n_accept++;
+    }
+    t = tf;
+    if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  } else {
+    T h = (T)std::min(o.dt, o.tf - o.t0);
+    T q_old = (T)C.qold_floor;
+    int64_t attempts = 0;
+    while (t < tf) {
+      if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
+      const bool last = (t + h >= tf);
+      if (last) h = tf - t;
+      ++attempts;
+      if (!ros23_step<T>(model, n, p, t, h, u, F0, unew, F2, k1, k2, E)) {
+        h = h * T(0.5);                                   // singular W: reject, halve (DESIGN R10)
+        tr.n_reject++;
+        if (t + h == t) { tr.retcode = RET_SINGULAR; break; }
+        continue;
+      }
+      const T q = error_q<T>(n, E, u, unew, abstol, reltol);
+      if (q < T(1)) {
+        const T tn = last ? tf : t + h;
+        while (js < k && tau[js] <= tn) {
+          if (tau[js] == tn) put(tr.save, n, js, unew);
+          else { T out[8]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
+          ++js;
+        }
+        t = tn;
+        for (int j = 0; j < n; ++j) { u[j] = unew[j]; F0[j] = F2[j]; }
+        tr.n_accept++;
+        h = pi_accept<T>(C, h, q, &q_old);
+      } else {
+        h = pi_reject<T>(C, h, q);
+        tr.n_reject++;
+      }
+      if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
+    }
+  }
+  if (k == 0) put(tr.save, n, 0, u);
+  else {
+    const T nan = std::numeric_limits<T>::quiet_NaN();
+    T nv[8]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    for (; js < k; ++js) put(tr.save, n, js, nv);
+  }
+}
+
+// --------------------------------------------------------- Euler–Maruyama ----
+// u_{i+1} = u_i + h a(u_i,t_i) + b(u_i,t_i) ⊙ ΔW_i, ΔW_i = √h Z_i ~ N(0, h I)
+// (P:153-157). Fixed grid (DESIGN R3); saveat on grid points (DESIGN R11).
+template <class T>
+static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+  const int n = tr.n, model = o.model;
+  T u[8], a[8], b[8], z[3];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  int64_t nsteps; double h_last;
+  fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+  const T hdt = (T)o.dt, hl = (T)h_last;
+  const T sq_dt = std::sqrt(hdt), sq_l = std::sqrt(hl);
+  int js = 0;
+  const int k = o.k;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; }
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const bool last = (i == nsteps - 1);
+    const T h = last ? hl : hdt, sh = last ? sq_l : sq_dt;
+    const T t = (T)(o.t0 + (double)i * o.dt);
+    rhs<T>(model, u, p, t, a);
+    diffusion<T>(model, u, p, t, b);
+    normals3<T>(o.seed, (uint64_t)i, tr.gidx, z);
+    for (int j = 0; j < n; ++j) {
+      const T dW = sh * z[j];
+      u[j] = std::fma(b[j], dW, std::fma(h, a[j], u[j]));
+    }
+    tr.n_accept++;
+    while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
+  }
+  if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  if (k == 0) put(tr.save, n, 0, u);
+}
+
+// ------------------------------------------------------------- driver ----
+// Solves trajectories one after another (the plain loop of CS-6). Inputs and
+// outputs use the SoA layout of include/ens.h (component-major, trajectory
+// fastest) so that tests can hand the same buffers to both sides.
+template <class T>
+static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_broadcast,
+                     const uint64_t* gidx, T* u_out, int32_t* retcode, int32_t* nacc, int32_t* nrej) {
+  Dims d;
+  if (!dims(o.model, &d)) return 1;
+  const int n = d.n, m = d.m, k = o.k;
+  // EM save points as step indices (DESIGN R11)
+  std::vector<int64_t> save_step(k);
+  if (o.alg == EM) {
+    for (int j = 0; j < k; ++j) save_step[j] = (int64_t)std::nearbyint((o.saveat[j] - o.t0) / o.dt);
+  }
+  const int kk = std::max(k, 1);
+  std::vector<T> buf((size_t)kk * n);
+  for (int64_t i = 0; i < N; ++i) {
+    Traj<T> tr;
+    tr.n = n; tr.m = m;
+    for (int j = 0; j < n; ++j) tr.u0[j] = u0[(size_t)j * N + i];
+    for (int j = 0; j < m; ++j) tr.p[j] = p_broadcast ? p[j] : p[(size_t)j * N + i];
+    tr.gidx = gidx ? gidx[i] : (uint64_t)i;
+    tr.save = buf.data();
+    if (o.alg == TSIT5) solve_tsit5<T>(o, tr);
+    else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
+    else solve_em<T>(o, tr, save_step.data());
+    for (int s = 0; s < kk; ++s)
+      for (int j = 0; j < n; ++j) u_out[((size_t)s * n + j) * N + i] = buf[(size_t)s * n + j];
+    if (retcode) retcode[i] = tr.retcode;
+    if (nacc) nacc[i] = tr.n_accept;
+    if (nrej) nrej[i] = tr.n_reject;
+  }
+  return 0;
+}
+
+}  // namespace orc
+
+// =========================================================== C interface ====
+extern "C" {
+
+int orc_model_dims(int model, int* n, int* m, int* nw) {
+  orc::Dims d;
+  if (!orc::dims(model, &d)) return 1;
+  *n = d.n; *m = d.m; *nw = d.nw;
+  return 0;
+}
+
+// dtype: 0 = f32, 1 = f64 (mirrors include/ens.h).
+int orc_rhs(int model, int dtype, const void* u, const void* p, double t, void* f) {
+  if (dtype == 0) orc::rhs<float>(model, (const float*)u, (const float*)p, (float)t, (float*)f);
+  else orc::rhs<double>(model, (const double*)u, (const double*)p, t, (double*)f);
+  return 0;
+}
+int orc_jac(int model, int dtype, const void* u, const void* p, double t, void* J) {
+  if (dtype == 0) orc::jac<float>(model, (const float*)u, (const float*)p, (float)t, (float*)J);
+  else orc::jac<double>(model, (const double*)u, (const double*)p, t, (double*)J);
+  return 0;
+}
+int orc_diffusion(int model, int dtype, const void* u, const void* p, double t, void* b) {
+  if (dtype == 0) orc::diffusion<float>(model, (const float*)u, (const float*)p, (float)t, (float*)b);
+  else orc::diffusion<double>(model, (const double*)u, (const double*)p, t, (double*)b);
+  return 0;
+}
+
+// Tableau export for the invariant pins: c[7], A[49] row-major, btilde[7], r[28].
+void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
+  for (int i = 0; i < 7; ++i) {
+    c[i] = orc::TS_C[i]; btilde[i] = orc::TS_BTILDE[i];
+    for (int j = 0; j < 7; ++j) A[i * 7 + j] = orc::TS_A[i][j];
+    for (int j = 0; j < 4; ++j) r[i * 4 + j] = orc::TS_R[i][j];
+  }
+}
+void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
+void orc_controller(int alg, double* out6) {
+  const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
+  out6[0] = C.beta1; out6[1] = C.beta2; out6[2] = C.eta; out6[3] = C.qmin_inv; out6[4] = C.qmax_inv;
+  out6[5] = C.qold_floor;
+}
+
+// Controller / error-norm pins (fp64): returns h_new; *q_old updated on accept.
+double orc_pi(int alg, int accept, double h, double q, double* q_old) {
+  const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
+  return accept ? orc::pi_accept<double>(C, h, q, q_old) : orc::pi_reject<double>(C, h, q);
+}
+double orc_error_q(int n, const double* E, const double* u, const double* unew, double abstol, double reltol) {
+  return orc::error_q<double>(n, E, u, unew, abstol, reltol);
+}
+
+void orc_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  orc::philox4x32_10(ctr, key, out);
+}
+void orc_uniforms(int dtype, const uint32_t* w4, void* out) {
+  if (dtype == 0) for (int i = 0; i < 4; ++i) ((float*)out)[i] = orc::u01_f32(w4[i]);
+  else { ((double*)out)[0] = orc::u01_f64(w4[0], w4[1]); ((double*)out)[1] = orc::u01_f64(w4[2], w4[3]); }
+}
+// Normals for `count` consecutive steps of trajectory gidx: out[count][3].
+void orc_normals(int dtype, uint64_t seed, uint64_t gidx, int64_t step0, int64_t count, void* out) {
+  for (int64_t s = 0; s < count; ++s) {
+    if (dtype == 0) orc::normals3<float>(seed, (uint64_t)(step0 + s), gidx, (float*)out + 3 * s);
+    else orc::normals3<double>(seed, (uint64_t)(step0 + s), gidx, (double*)out + 3 * s);
+  }
+}
+
+void orc_fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last) {
+  orc::fixed_grid(t0, tf, dt, nsteps, h_last);
+}
+
+// LU pins: factor + solve one system (row-major A, n ≤ 8). Returns 0 ok, 1 singular.
+int orc_lu_solve(int dtype, int n, const void* A, const void* b, void* x) {
+  int piv[8];
+  if (dtype == 0) {
+    float W[64], inv[8]; std::memcpy(W, A, sizeof(float) * n * n);
+    if (!orc::lu_factor<float>(n, W, piv, inv)) return 1;
+    orc::lu_solve<float>(n, W, piv, inv, (const float*)b, (float*)x);
+  } else {
+    double W[64], inv[8]; std::memcpy(W, A, sizeof(double) * n * n);
+    if (!orc::lu_factor<double>(n, W, piv, inv)) return 1;
+    orc::lu_solve<double>(n, W, piv, inv, (const double*)b, (double*)x);
+  }
+  return 0;
+}
+
+// Whole-ensemble solve. u0: [n][N], p: [m][N] (or [m] if p_broadcast),
+// gidx: [N] global indices (NULL → 0..N-1), u_out: [max(k,1)][n][N].
+int orc_solve(int model, int alg, int dtype, int64_t N, const void* u0, const void* p, int p_broadcast,
+              const uint64_t* gidx, double t0, double tf, double dt, int adaptive, double abstol,
+              double reltol, int64_t max_steps, uint64_t seed, const double* saveat, int k,
+              void* u_out, int32_t* retcode, int32_t* n_accept, int32_t* n_reject) {
+  orc::Opts o;
+  o.model = model; o.alg = alg; o.adaptive = adaptive; o.t0 = t0; o.tf = tf; o.dt = dt;
+  o.abstol = abstol; o.reltol = reltol; o.max_steps = max_steps > 0 ? max_steps : 1000000;
+  o.seed = seed; o.saveat = saveat; o.k = k;
+  if (dtype == 0)
+    return orc::solve_all<float>(o, N, (const float*)u0, (const float*)p, p_broadcast, gidx,
+                                 (float*)u_out, retcode, n_accept, n_reject);
+  return orc::solve_all<double>(o, N, (const double*)u0, (const double*)p, p_broadcast, gidx,
+                                (double*)u_out, retcode, n_accept, n_reject);
+}
+
+// Ensemble statistics ("mean and variance"; DESIGN R12): two-pass in
+// long double over trajectories with mask[i] != 0 (mask NULL → all), unbiased
+// variance (N−1). x: [k][n][N] in T; mean/var: [k][n] fp64; count out.
+int orc_stats(int dtype, int64_t N, int k, int n, const void* x, const int32_t* mask,
+              double* mean, double* var, int64_t* count) {
+  for (int s = 0; s < k; ++s)
+    for (int j = 0; j < n; ++j) {
+      const size_t off = ((size_t)s * n + j) * N;
+      long double sum = 0; int64_t c = 0;
+      for (int64_t i = 0; i < N; ++i) {
+        if (mask && !mask[i]) continue;
+        const long double v = dtype == 0 ? (long double)((const float*)x)[off + i]
+                                         : (long double)((const double*)x)[off + i];
+        sum += v; ++c;
+      }
+      const long double mu = c ? sum / c : 0;
+      long double ss = 0;
+      for (int64_t i = 0; i < N; ++i) {
+        if (mask && !mask[i]) continue;
+        const long double v = dtype == 0 ? (long double)((const float*)x)[off + i]
+                                         : (long double)((const double*)x)[off + i];
+        ss += (v - mu) * (v - mu);
+      }
+      mean[s * n + j] = (double)mu;
+      var[s * n + j] = c > 1 ? (double)(ss / (c - 1)) : 0.0;
+      if (count) *count = c;
+    }
+  return 0;
+}
+
+}  // extern "C"
