@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark: trajectories/s of a Lorenz Tsit5 ensemble on B200 (BASELINE.json
+metric; configs[1] headline point: N=10^7, fixed dt=1e-3 on [0,1] → 1000 steps,
+fp32, ρ sweep over (0,21] as in P:400).
+
+One step = one whole pass of the hot path over the batch: ensemble_solve (a2–a7,
+a13: one kernel, one thread per trajectory) + ensemble statistics of the final
+states (a12) + for N>1 GPUs the cross-GPU exchange (a14: NCCL all-gather of the
+statistics triples + fixed-order merge, and NCCL gather of the final states to
+rank 0). Inputs are generated on device before the timed region (resident in
+HBM); they (240 MB) plus the outputs exceed the 126 MB L2, so no flush is needed.
+
+Usage:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FP32_LANES_PER_SM = 128     # FFMA lanes per SM (B200 profiling guide; tools/peaks.cu measured 121-126/clk)
+FP64_LANES_PER_SM = 64
+SM_MAX_MHZ = 1965.0
+METRIC = "trajectories/sec (Lorenz Tsit5, fp32/fp64) at 1/2/4/8 B200; % FP peak"
+
+
+def flops_per_traj(nsteps: int) -> float:
+    """Algorithmic FLOPs of one fixed-step Tsit5 Lorenz trajectory:
+    per step 48n (stage sums, n=3) + 6F (six RHS, F=8) = 192; plus f(u0) = 8."""
+    return 192.0 * nsteps + 8.0
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period: float = 0.05):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline(N: int, nsteps_dt: float, sample: int, threads: int) -> dict:
+    """The oracle as it stands (single-threaded C++ per call) over a bounded
+    sample of the same workload, spread over host threads by a harness pool
+    (ctypes releases the GIL during each oracle call)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle
+    from synth.inputs import make_inputs
+    u0, p = make_inputs("lorenz", "rho_sweep", N, dtype="f32")
+    idx = np.linspace(0, N - 1, sample).astype(np.int64)      # spread over the ρ sweep
+    u0s, ps = np.ascontiguousarray(u0[:, idx]), np.ascontiguousarray(p[:, idx])
+    chunks = np.array_split(np.arange(sample), threads * 4)
+
+    def work(c):
+        oracle.solve("lorenz", "tsit5", u0s[:, c], ps[:, c], (0.0, 1.0), nsteps_dt, dtype="f32")
+
+    oracle.lib()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, chunks))
+    wall = time.perf_counter() - t0
+    return {"value": sample / wall, "unit": "trajectories/s", "cores": threads, "kind": "oracle",
+            "sample": f"{sample} Lorenz Tsit5 fixed-dt fp32 trajectories (1000 steps each) spread over the "
+                      f"N={N} rho sweep; {threads} host threads; wall {wall:.2f} s"}
+
+
+def load_traffic(tag: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(f.read_text())
+        e = d.get(tag)
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, rank):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    N = args.n
+    vals = []
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_baseline(N, 1e-3, max(threads, sample // 8), threads)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(N, 1e-3, sample, threads))
+    v = statistics.median([x["value"] for x in vals])
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "trajectories/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"lorenz_tsit5_fixed_dt1e-3_fp32_N{N}_rho_sweep (oracle sample per step)",
+                       "N_per_gpu": N, "sample_per_step": sample},
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": "trajectories/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=10**7, help="trajectories per GPU")
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=24576)
+    ap.add_argument("--ref-sample", type=int, default=16384)
+    ap.add_argument("--no-gather", action="store_true", help="skip the NCCL gather of final states (N>1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2304_06835_b200 as ens
+    from paper_2304_06835_b200 import multi_gpu as mg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    N = args.n
+    shard = mg.shard_weak(N, rank, world)
+    N_total = N * world
+    tspan, dt = (0.0, 1.0), 1e-3
+    nsteps = 1000
+
+    # a1: inputs generated on device from (seed, global index) — no host scatter
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=tdt, index_offset=shard.index_offset,
+                                N_total=N_total, device=dev)
+    sol = ens.Solution(u=torch.empty((3, N), dtype=tdt, device=dev),
+                       retcode=torch.empty(N, dtype=torch.int32, device=dev),
+                       n_accept=torch.empty(N, dtype=torch.int32, device=dev),
+                       n_reject=torch.empty(N, dtype=torch.int32, device=dev), stats=None)
+    ws = ens.Workspace(ens.workspace_bytes("lorenz", "tsit5", tdt, N), dev)
+    sws = ens.Workspace(ens.lib().ens_stats_workspace_bytes(N, 3), dev)
+    st_local = torch.empty((1, 3, 3), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    launches_per_step = [0]
+
+    def step(ev_k0=None, ev_k1=None):
+        n_l = 0
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        ens.solve("lorenz", "tsit5", u0, p, tspan, dt, workspace=ws, out=sol, stream=stream)
+        n_l += 1
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+        ens.ensemble_stats(sol.u.view(1, 3, N), out=st_local, workspace=sws, stream=stream)
+        n_l += 2
+        if world > 1:
+            g = mg.allgather_stats(st_local)
+            mg.merge_stats(g)
+            n_l += 1
+            if not args.no_gather:
+                mg.gather_states(sol.u)
+        launches_per_step[0] = n_l
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for s in range(args.steps):
+            step(*kev[s])
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    k_ms = [a.elapsed_time(b) for a, b in kev]
+    k_avg = sum(k_ms) / len(k_ms)
+    t = torch.tensor([ms, k_avg], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, k_max = t.tolist()
+    assert (sol.retcode == 0).all().item(), "non-success retcodes in the benchmark ensemble"
+
+    # end to end through the C ABI on host buffers (pinned), copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        from synth.inputs import make_inputs
+        u0h_np, ph_np = make_inputs("lorenz", "rho_sweep", N, dtype=args.dtype, index_offset=shard.index_offset,
+                                    N_total=N_total)
+        u0h = torch.from_numpy(u0h_np).pin_memory()
+        ph = torch.from_numpy(ph_np).pin_memory()
+        uo = torch.empty((1, 3, N), dtype=tdt, pin_memory=True)
+        rco = torch.empty(N, dtype=torch.int32, pin_memory=True)
+        staging = None
+        for _ in range(2):
+            _, _, staging = ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=8,
+                                           staging=staging, u_out_host=uo, retcode_host=rco)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=8, staging=staging,
+                           u_out_host=uo, retcode_host=rco)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        tsz = 4 if args.dtype == "f32" else 8
+        e2e = {"value": N_total * args.steps / el.item(), "unit": "trajectories/s",
+               "h2d_bytes_per_step": (3 + 3) * tsz * N, "d2h_bytes_per_step": 3 * tsz * N + 4 * N,
+               "api": "ensemble_solve_host (pinned host buffers, 8 chunks, H2D/compute/D2H overlapped)",
+               "per_rank_bytes": True}
+
+    if rank == 0:
+        value = N_total * args.steps / (ms_max / 1e3)
+        lanes = FP32_LANES_PER_SM if args.dtype == "f32" else FP64_LANES_PER_SM
+        props = torch.cuda.get_device_properties(dev)
+        peak = props.multi_processor_count * lanes * 2 * SM_MAX_MHZ * 1e6 / 1e12
+        achieved = N * flops_per_traj(nsteps) / (k_max / 1e3) / 1e12
+        tag = f"tsit5_fixed_lorenz_{args.dtype}"
+        line = {
+            "metric": METRIC, "value": value, "unit": "trajectories/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"lorenz_tsit5_fixed_dt1e-3_{args.dtype}_rho_sweep (BASELINE configs[1] headline "
+                                   f"point, N=10^7 per GPU)",
+                       "N_per_gpu": N, "N_total": N_total, "tspan": [0.0, 1.0], "dt": dt, "nsteps": nsteps,
+                       "parallelism": f"dp{world} (trajectory shards)", "l2": "inputs+outputs (360 MB) > L2 (126 MB)",
+                       "step": "ensemble_solve + ensemble_stats" + (" + NCCL allgather(stats)+merge" +
+                                                                    ("" if args.no_gather else " + NCCL gather(states)")
+                                                                    if world > 1 else "")},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": load_traffic(tag),
+                         "kernel": f"tsit5_fixed_kernel<Lorenz,{'float' if args.dtype == 'f32' else 'double'}>",
+                         "kernel_ms": k_max, "flop_per_traj": flops_per_traj(nsteps),
+                         "peak_basis": f"{props.multi_processor_count} SMs x {lanes} FMA lanes x 2 x {SM_MAX_MHZ:.0f} MHz",
+                         "kernel_share_of_step": k_max / (ms_max / args.steps)},
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step[0] * args.steps,
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(N_total, dt, args.cpu_sample, os.cpu_count() or 1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

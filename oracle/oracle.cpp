@@ -645,7 +645,11 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
   if (o.alg == EM) {
-    for (int j = 0; j < k; ++j) save_step[j] = (int64_t)std::nearbyint((o.saveat[j] - o.t0) / o.dt);
+    // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    for (int j = 0; j < k; ++j)
+      save_step[j] = (o.saveat[j] == o.tf) ? nsteps : (int64_t)std::nearbyint((o.saveat[j] - o.t0) / o.dt);
   }
   const int kk = std::max(k, 1);
   std::vector<T> buf((size_t)kk * n);
@@ -773,8 +777,8 @@ int orc_solve(int model, int alg, int dtype, int64_t N, const void* u0, const vo
 }
 
 // Ensemble statistics ("mean and variance"; DESIGN R12): two-pass in
-// long double over trajectories with mask[i] != 0 (mask NULL → all), unbiased
-// variance (N−1). x: [k][n][N] in T; mean/var: [k][n] fp64; count out.
+// long double over the finite values of trajectories with mask[i] != 0 (mask
+// NULL → all), unbiased variance (N−1). x: [k][n][N] in T; mean/var: [k][n] fp64; count out.
 int orc_stats(int dtype, int64_t N, int k, int n, const void* x, const int32_t* mask,
               double* mean, double* var, int64_t* count) {
   for (int s = 0; s < k; ++s)
@@ -785,6 +789,7 @@ int orc_stats(int dtype, int64_t N, int k, int n, const void* x, const int32_t* 
         if (mask && !mask[i]) continue;
         const long double v = dtype == 0 ? (long double)((const float*)x)[off + i]
                                          : (long double)((const double*)x)[off + i];
+        if (!std::isfinite(v)) continue;          // DESIGN R12: finite values only
         sum += v; ++c;
       }
       const long double mu = c ? sum / c : 0;
@@ -793,6 +798,7 @@ int orc_stats(int dtype, int64_t N, int k, int n, const void* x, const int32_t* 
         if (mask && !mask[i]) continue;
         const long double v = dtype == 0 ? (long double)((const float*)x)[off + i]
                                          : (long double)((const double*)x)[off + i];
+        if (!std::isfinite(v)) continue;
         ss += (v - mu) * (v - mu);
       }
       mean[s * n + j] = (double)mu;

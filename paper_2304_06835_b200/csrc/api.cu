@@ -1,0 +1,473 @@
+// api.cu — C ABI of the ensemble solver (include/ens.h): argument validation,
+// workspace layout, dispatch over the template instances <Model, T, alg,
+// adaptive, saveat, scheduler>, launch configuration, host end-to-end pipeline.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ens.h"
+#include "common.cuh"
+#include "em.cuh"
+#include "inputs.cuh"
+#include "models.cuh"
+#include "ros23.cuh"
+#include "sched.cuh"
+#include "stats.cuh"
+#include "tsit5.cuh"
+
+using namespace ens;
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int64_t kStatsChunk = 8192;
+
+bool model_dims(int model, int* n, int* m, int* nw) {
+  switch (model) {
+    case ENS_LORENZ: case ENS_ROBERTSON: *n = 3; *m = 3; *nw = 0; return true;
+    case ENS_LORENZ_SDE_ADD: case ENS_LORENZ_SDE_MUL: *n = 3; *m = 4; *nw = 3; return true;
+    case ENS_GBM: *n = 3; *m = 2; *nw = 3; return true;
+    case ENS_EXPDECAY: *n = 1; *m = 1; *nw = 0; return true;
+    case ENS_HARMONIC: *n = 2; *m = 1; *nw = 0; return true;
+  }
+  return false;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// DESIGN R3: fixed-step count and last step, in fp64.
+void fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last) {
+  const double r = (tf - t0) / dt;
+  const double rr = std::nearbyint(r);
+  int64_t ns = (std::fabs(r - rr) <= 1e-9 * std::max(1.0, r)) ? (int64_t)rr : (int64_t)std::ceil(r);
+  if (ns < 1) ns = 1;
+  *nsteps = ns;
+  *h_last = (tf - t0) - (double)(ns - 1) * dt;
+}
+
+struct Layout {
+  size_t counter, tau, save_step, partial, total;
+  int64_t nparts;
+  int rows;
+};
+
+Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
+  Layout L{};
+  const int k = opt ? std::max(0, opt->n_saveat) : 0;
+  const size_t tsz = dtype == ENS_F32 ? 4 : 8;
+  L.counter = 0;
+  L.tau = 256;
+  L.save_step = L.tau + align256(std::max(1, k) * tsz);
+  L.partial = L.save_step + align256(std::max(1, k) * 8);
+  L.rows = std::max(1, k) * n;
+  const bool stats = opt && opt->want_stats;
+  L.nparts = 0;
+  if (stats) L.nparts = (alg == ENS_EM) ? cdiv(N, kBlock) : cdiv(N, kStatsChunk);
+  L.total = L.partial + align256((size_t)L.rows * (size_t)L.nparts * 3 * 8) + 256;
+  return L;
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+template <class K>
+ens_status launch_check() {
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+template <class T>
+dim3 grid_for(int64_t N) { return dim3((unsigned)cdiv(N, kBlock)); }
+
+// ---------------------------------------------------------------- dispatch --
+template <class M, class T>
+ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  const bool save = a.k > 0;
+  const dim3 g = grid_for<T>(a.N), b(kBlock);
+  if (alg == ENS_TSIT5) {
+    if (!opt->adaptive) {
+      if (save) tsit5_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
+      else tsit5_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    } else if (opt->refill) {
+      int occ = 0;
+      if (save) {
+        auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, true>, T>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        kern<<<gr, b, 0, s>>>(a);
+      } else {
+        auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, false>, T>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        kern<<<gr, b, 0, s>>>(a);
+      }
+    } else {
+      if (save) adaptive_static_kernel<Tsit5Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
+      else adaptive_static_kernel<Tsit5Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
+    }
+  } else {  // Rosenbrock23
+    if (!opt->adaptive) {
+      if (save) ros23_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
+      else ros23_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    } else if (opt->refill) {
+      int occ = 0;
+      if (save) {
+        auto kern = adaptive_refill_kernel<Ros23Lane<M, T, true>, T>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        kern<<<gr, b, 0, s>>>(a);
+      } else {
+        auto kern = adaptive_refill_kernel<Ros23Lane<M, T, false>, T>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        kern<<<gr, b, 0, s>>>(a);
+      }
+    } else {
+      if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
+      else adaptive_static_kernel<Ros23Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
+    }
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+template <class M, class T>
+ens_status run_sde(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  const dim3 g = grid_for<T>(a.N), b(kBlock);
+  if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
+  else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+template <class T>
+ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  switch (model) {
+    case ENS_LORENZ: return run_ode<Lorenz, T>(alg, a, opt, s);
+    case ENS_ROBERTSON: return run_ode<Robertson, T>(alg, a, opt, s);
+    case ENS_EXPDECAY: return run_ode<ExpDecay, T>(alg, a, opt, s);
+    case ENS_HARMONIC: return run_ode<Harmonic, T>(alg, a, opt, s);
+    case ENS_LORENZ_SDE_ADD: return run_sde<LorenzSDE<false>, T>(a, opt, s);
+    case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(a, opt, s);
+    case ENS_GBM: return run_sde<GBM, T>(a, opt, s);
+  }
+  return ENS_E_INVALID_ARG;
+}
+
+// Validation shared by ensemble_solve and ensemble_solve_host.
+ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double tf, double dt,
+                    const ens_options* opt, int* n_out) {
+  int n, m, nw;
+  if (!opt || N < 1 || !model_dims(model, &n, &m, &nw)) return ENS_E_INVALID_ARG;
+  if (alg < ENS_TSIT5 || alg > ENS_EM || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
+  if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
+  const bool sde = nw > 0;
+  if (sde != (alg == ENS_EM)) return ENS_E_ALG_MISMATCH;
+  if (alg == ENS_EM && opt->adaptive) return ENS_E_ADAPTIVE_UNSUPPORTED;
+  if (!std::isfinite(t0) || !std::isfinite(tf) || !std::isfinite(dt) || !(t0 < tf) || !(dt > 0))
+    return ENS_E_BAD_TSPAN;
+  if (opt->adaptive) {
+    if (!std::isfinite(opt->abstol) || !std::isfinite(opt->reltol) || !(opt->abstol > 0) || !(opt->reltol >= 0))
+      return ENS_E_BAD_TOLERANCE;
+  }
+  const int k = opt->n_saveat;
+  for (int j = 0; j < k; ++j) {
+    const double tj = opt->saveat[j];
+    if (!std::isfinite(tj) || tj < t0 || tj > tf) return ENS_E_BAD_SAVEAT;
+    if (j > 0 && !(tj > opt->saveat[j - 1])) return ENS_E_BAD_SAVEAT;
+    if (j > 0) {   // strictly increasing also after the cast to T
+      if (dtype == ENS_F32 && !((float)tj > (float)opt->saveat[j - 1])) return ENS_E_BAD_SAVEAT;
+    }
+  }
+  *n_out = n;
+  return ENS_OK;
+}
+
+// EM save points as grid indices (DESIGN R11): τ must be t0 + s·dt (s < nsteps) or tf.
+bool em_save_steps(double t0, double tf, double dt, const double* sa, int k, std::vector<int64_t>& out) {
+  int64_t nsteps; double hl;
+  fixed_grid(t0, tf, dt, &nsteps, &hl);
+  out.resize(k);
+  for (int j = 0; j < k; ++j) {
+    int64_t s;
+    if (sa[j] == tf) s = nsteps;
+    else {
+      s = (int64_t)std::nearbyint((sa[j] - t0) / dt);
+      if (s < 0 || s >= nsteps) return false;
+      if (std::fabs(t0 + (double)s * dt - sa[j]) > 1e-9 * std::max(1.0, std::fabs(sa[j]))) return false;
+    }
+    if (j > 0 && s <= out[j - 1]) return false;
+    out[j] = s;
+  }
+  return true;
+}
+
+template <class T>
+ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0, const void* p, double t0,
+                      double tf, double dt, const ens_options* opt, const ens_output* out, int n,
+                      cudaStream_t s, bool stage_ws) {
+  const Layout L = layout(n, alg, sizeof(T) == 4 ? ENS_F32 : ENS_F64, N, opt);
+  char* ws = (char*)out->workspace;
+  Args<T> a{};
+  a.N = N; a.ld = ld;
+  a.u0 = (const T*)u0; a.p = (const T*)p; a.p_broadcast = opt->p_broadcast;
+  a.t0d = t0; a.tfd = tf; a.dtd = dt;
+  a.t0 = (T)t0; a.tf = (T)tf;
+  int64_t nsteps; double hl;
+  fixed_grid(t0, tf, dt, &nsteps, &hl);
+  a.nsteps = nsteps; a.h_last = (T)hl;
+  a.dt0 = opt->adaptive ? (T)std::min(dt, tf - t0) : (T)dt;
+  a.abstol = (T)opt->abstol; a.reltol = (T)opt->reltol;
+  a.max_steps = opt->max_steps > 0 ? opt->max_steps : 1000000;
+  a.k = opt->n_saveat;
+  a.tau = (const T*)(ws + L.tau);
+  a.save_step = (const int64_t*)(ws + L.save_step);
+  a.u_out = (T*)out->u_out; a.retcode = out->retcode; a.nacc = out->n_accept; a.nrej = out->n_reject;
+  a.seed = opt->seed; a.index_offset = opt->index_offset; a.chunk_len = opt->chunk_len;
+  a.chunk_stride = opt->chunk_stride;
+  a.partial = (double*)(ws + L.partial);
+  a.counter = (unsigned long long*)(ws + L.counter);
+  if (stage_ws) {
+    if (a.k > 0) {
+      std::vector<T> tau(a.k);
+      for (int j = 0; j < a.k; ++j) tau[j] = (T)opt->saveat[j];
+      if (cudaMemcpyAsync(ws + L.tau, tau.data(), sizeof(T) * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return ENS_E_CUDA;
+      if (alg == ENS_EM) {
+        std::vector<int64_t> st;
+        if (!em_save_steps(t0, tf, dt, opt->saveat, a.k, st)) return ENS_E_BAD_SAVEAT;
+        if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
+          return ENS_E_CUDA;
+      }
+    }
+  }
+  if (opt->adaptive && opt->refill) {
+    if (cudaMemsetAsync(ws + L.counter, 0, 8, s) != cudaSuccess) return ENS_E_CUDA;
+  }
+  ens_status st = dispatch<T>(model, alg, a, opt, s);
+  if (st != ENS_OK) return st;
+  if (opt->want_stats) {
+    if (alg != ENS_EM) {
+      const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
+      stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, kStatsChunk, a.partial);
+    }
+    stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)L.nparts, out->stats);
+    if (cudaPeekAtLastError() != cudaSuccess) return ENS_E_CUDA;
+  }
+  return ENS_OK;
+}
+
+}  // namespace
+
+// =============================================================== C ABI =====
+extern "C" {
+
+ens_status ens_model_dims(ens_model model, int32_t* n, int32_t* m, int32_t* nw) {
+  int a, b, c;
+  if (!model_dims(model, &a, &b, &c)) return ENS_E_INVALID_ARG;
+  if (n) *n = a;
+  if (m) *m = b;
+  if (nw) *nw = c;
+  return ENS_OK;
+}
+
+size_t ens_workspace_bytes(ens_model model, ens_alg alg, ens_dtype dtype, int64_t N, const ens_options* opt) {
+  int n, m, nw;
+  if (!model_dims(model, &n, &m, &nw)) return 0;
+  return layout(n, alg, dtype, N, opt).total;
+}
+
+ens_status ensemble_solve(ens_model model, ens_alg alg, ens_dtype dtype, int64_t N, const void* u0, const void* p,
+                          double t0, double tf, double dt, const ens_options* opt, ens_output* out, void* stream) {
+  int n = 0;
+  ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
+  if (st != ENS_OK) return st;
+  if (!out || !u0 || !p) return ENS_E_INVALID_ARG;
+  if (!out->u_out && !(alg == ENS_EM && opt->want_stats)) return ENS_E_INVALID_ARG;
+  if (opt->want_stats && !out->stats) return ENS_E_INVALID_ARG;
+  if (alg == ENS_EM && opt->n_saveat > 0) {
+    std::vector<int64_t> tmp;
+    if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
+  }
+  if (!out->workspace || out->workspace_bytes < ens_workspace_bytes(model, alg, dtype, N, opt)) return ENS_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == ENS_F32) return solve_impl<float>(model, alg, N, N, u0, p, t0, tf, dt, opt, out, n, s, true);
+  return solve_impl<double>(model, alg, N, N, u0, p, t0, tf, dt, opt, out, n, s, true);
+}
+
+ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, int64_t N, const void* u0_host,
+                               const void* p_host, double t0, double tf, double dt, const ens_options* opt,
+                               void* d_u0, void* d_p, void* d_u_out, int32_t* d_retcode, void* u_out_host,
+                               int32_t* retcode_host, void* workspace, size_t workspace_bytes, int32_t n_chunks,
+                               void* stream) {
+  int n = 0, m = 0, nw = 0;
+  ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
+  if (st != ENS_OK) return st;
+  if (alg == ENS_EM || opt->want_stats) return ENS_E_UNSUPPORTED;
+  if (!u0_host || !p_host || !d_u0 || !d_p || !d_u_out || !u_out_host) return ENS_E_INVALID_ARG;
+  if (!workspace || workspace_bytes < ens_workspace_bytes(model, alg, dtype, N, opt)) return ENS_E_WORKSPACE;
+  model_dims(model, &n, &m, &nw);
+  const size_t ts = dtype == ENS_F32 ? 4 : 8;
+  const int kk = std::max(1, opt->n_saveat);
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(n_chunks, N));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t sh = nullptr, sd = nullptr;
+  if (cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking) != cudaSuccess) return ENS_E_CUDA;
+  if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) { cudaStreamDestroy(sh); return ENS_E_CUDA; }
+  std::vector<cudaEvent_t> ev_in(C), ev_out(C);
+  for (int64_t c = 0; c < C; ++c) {
+    cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming);
+  }
+  ens_output out{};
+  out.workspace = workspace; out.workspace_bytes = workspace_bytes;
+  bool ok = true;
+  // stage saveat once (stream-ordered on s)
+  cudaEvent_t start;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventRecord(start, s);
+  cudaStreamWaitEvent(sh, start, 0);
+  const int64_t base = N / C, rem = N % C;
+  int64_t lo = 0;
+  for (int64_t c = 0; c < C && ok; ++c) {
+    const int64_t len = base + (c < rem ? 1 : 0);
+    // H2D of chunk c (component rows are strided by N in the SoA layout)
+    ok &= cudaMemcpy2DAsync((char*)d_u0 + lo * ts, N * ts, (const char*)u0_host + lo * ts, N * ts, len * ts, n,
+                            cudaMemcpyHostToDevice, sh) == cudaSuccess;
+    if (opt->p_broadcast) {
+      if (c == 0) ok &= cudaMemcpyAsync(d_p, p_host, m * ts, cudaMemcpyHostToDevice, sh) == cudaSuccess;
+    } else {
+      ok &= cudaMemcpy2DAsync((char*)d_p + lo * ts, N * ts, (const char*)p_host + lo * ts, N * ts, len * ts, m,
+                              cudaMemcpyHostToDevice, sh) == cudaSuccess;
+    }
+    cudaEventRecord(ev_in[c], sh);
+    cudaStreamWaitEvent(s, ev_in[c], 0);
+    out.u_out = (char*)d_u_out + lo * ts;
+    out.retcode = d_retcode ? d_retcode + lo : nullptr;
+    ens_options o = *opt;
+    const void* pp = opt->p_broadcast ? d_p : (const void*)((const char*)d_p + lo * ts);
+    if (dtype == ENS_F32)
+      st = solve_impl<float>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, s, c == 0);
+    else
+      st = solve_impl<double>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, s, c == 0);
+    if (st != ENS_OK) { ok = false; break; }
+    cudaEventRecord(ev_out[c], s);
+    cudaStreamWaitEvent(sd, ev_out[c], 0);
+    ok &= cudaMemcpy2DAsync((char*)u_out_host + lo * ts, N * ts, (const char*)d_u_out + lo * ts, N * ts, len * ts,
+                            (size_t)kk * n, cudaMemcpyDeviceToHost, sd) == cudaSuccess;
+    if (retcode_host && d_retcode)
+      ok &= cudaMemcpyAsync(retcode_host + lo, d_retcode + lo, len * 4, cudaMemcpyDeviceToHost, sd) == cudaSuccess;
+    lo += len;
+  }
+  ok &= cudaStreamSynchronize(sd) == cudaSuccess;
+  ok &= cudaStreamSynchronize(s) == cudaSuccess;
+  cudaStreamSynchronize(sh);
+  for (int64_t c = 0; c < C; ++c) { cudaEventDestroy(ev_in[c]); cudaEventDestroy(ev_out[c]); }
+  cudaEventDestroy(start);
+  cudaStreamDestroy(sh);
+  cudaStreamDestroy(sd);
+  if (st != ENS_OK) return st;
+  return ok ? ENS_OK : ENS_E_CUDA;
+}
+
+ens_status ens_generate_inputs(ens_model model, ens_dtype dtype, ens_recipe recipe, uint64_t input_seed, int64_t N,
+                               int64_t N_total, const ens_options* opt, void* u0, void* p, void* stream) {
+  InputSpec sp{};
+  int nw;
+  if (!model_dims(model, &sp.n, &sp.m, &nw) || N < 1 || !u0 || !p) return ENS_E_INVALID_ARG;
+  if (recipe < ENS_RECIPE_RANDOM10 || recipe > ENS_RECIPE_CONST) return ENS_E_INVALID_ARG;
+  if (recipe == ENS_RECIPE_RHO_SWEEP && model != ENS_LORENZ) return ENS_E_UNSUPPORTED;
+  // p̄ and ū0 of DESIGN §6 (same table as synth/inputs.py)
+  static const double PB[7][4] = {{10.0, 28.0, 8.0 / 3.0, 0}, {0.04, 3e7, 1e4, 0}, {10.0, 28.0, 8.0 / 3.0, 0.1},
+                                  {10.0, 28.0, 8.0 / 3.0, 0.1}, {1.5, 0.01, 0, 0}, {1.0, 0, 0, 0}, {1.0, 0, 0, 0}};
+  static const double UB[7][3] = {{1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {0.1, 0.1, 0.1}, {1, 0, 0}, {1, 0, 0}};
+  for (int j = 0; j < 4; ++j) sp.pbar[j] = PB[model][j];
+  for (int j = 0; j < 3; ++j) sp.ubar[j] = UB[model][j];
+  sp.recipe = recipe;
+  sp.n_total = (double)(N_total > 0 ? N_total : N);
+  const int64_t off = opt ? opt->index_offset : 0, cl = opt ? opt->chunk_len : 0, cs = opt ? opt->chunk_stride : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 g((unsigned)cdiv(N, kBlock));
+  if (dtype == ENS_F32) generate_inputs_kernel<float><<<g, kBlock, 0, s>>>(sp, input_seed, N, off, cl, cs, (float*)u0, (float*)p);
+  else generate_inputs_kernel<double><<<g, kBlock, 0, s>>>(sp, input_seed, N, off, cl, cs, (double*)u0, (double*)p);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+size_t ens_stats_workspace_bytes(int64_t N, int32_t rows) {
+  if (N < 1 || rows < 1) return 0;
+  return align256((size_t)rows * (size_t)cdiv(N, kStatsChunk) * 3 * 8) + 256;
+}
+
+ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int32_t rows, double* stats,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  if (!x || !stats || N < 1 || rows < 1 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (!workspace || workspace_bytes < ens_stats_workspace_bytes(N, rows)) return ENS_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nparts = cdiv(N, kStatsChunk);
+  const dim3 g((unsigned)nparts, (unsigned)rows);
+  double* part = (double*)workspace;
+  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, kStatsChunk, part);
+  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, kStatsChunk, part);
+  stats_merge_kernel<<<rows, 256, 0, s>>>(part, (int)nparts, stats);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+ens_status ens_stats_finalize(const double* stats, int32_t k, int32_t n, double* mean, double* var, void* stream) {
+  if (!stats || !mean || !var || n < 1 || k < 0) return ENS_E_INVALID_ARG;
+  const int rows = std::max(1, k) * n;
+  stats_finalize_kernel<<<cdiv(rows, 128), 128, 0, (cudaStream_t)stream>>>(stats, rows, mean, var);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+ens_status ens_stats_merge(const double* gathered, int32_t R, int32_t k, int32_t n, double* merged, void* stream) {
+  if (!gathered || !merged || R < 1 || n < 1 || k < 0) return ENS_E_INVALID_ARG;
+  const int rows = std::max(1, k) * n;
+  stats_rank_merge_kernel<<<cdiv(rows, 128), 128, 0, (cudaStream_t)stream>>>(gathered, R, rows, merged);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps,
+                         const ens_options* opt, uint32_t* words, void* z, void* stream) {
+  if (N < 1 || nsteps < 0 || step0 < 0 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  const int64_t off = opt ? opt->index_offset : 0, cl = opt ? opt->chunk_len : 0, cs = opt ? opt->chunk_stride : 0;
+  const dim3 g((unsigned)cdiv(N, kBlock));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == ENS_F32) sde_noise_kernel<float><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
+  else sde_noise_kernel<double><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+ens_status ens_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int64_t N, void* stream) {
+  if (!ctr || !key || !out || N < 1) return ENS_E_INVALID_ARG;
+  philox_kernel<<<(unsigned)cdiv(N, kBlock), kBlock, 0, (cudaStream_t)stream>>>(ctr, key, out, N);
+  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
+}
+
+const char* ens_status_string(ens_status s) {
+  switch (s) {
+    case ENS_OK: return "ok";
+    case ENS_E_INVALID_ARG: return "invalid argument";
+    case ENS_E_ALG_MISMATCH: return "algorithm does not match the model kind (ODE vs SDE)";
+    case ENS_E_ADAPTIVE_UNSUPPORTED: return "adaptive stepping is not supported for this algorithm";
+    case ENS_E_BAD_TOLERANCE: return "bad tolerance (abstol must be > 0, reltol >= 0)";
+    case ENS_E_BAD_TSPAN: return "bad time span or step (need t0 < tf, dt > 0, all finite)";
+    case ENS_E_BAD_SAVEAT: return "bad saveat (must be strictly increasing in [t0, tf]; EM: on the step grid)";
+    case ENS_E_WORKSPACE: return "workspace missing or too small";
+    case ENS_E_UNSUPPORTED: return "unsupported combination";
+    case ENS_E_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* ens_version(void) { return "ens-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -455,6 +455,10 @@ def test_stats_exact_small_cases():
     assert mean[0, 0] == 1e8 + 2.5 and abs(var[0, 0] - 5 / 3) < 1e-9
     mean, var, c = oracle.stats(x, mask=np.array([1, 0, 1, 0]))
     assert mean[0, 0] == 2.0 and var[0, 0] == 2.0 and c == 2
+    # non-finite values (failed trajectories, unreached save points) are excluded
+    z = np.array([1.0, np.nan, 3.0, np.inf]).reshape(1, 1, 4)
+    mean, var, c = oracle.stats(z)
+    assert mean[0, 0] == 2.0 and var[0, 0] == 2.0 and c == 2
 
 
 # --------------------------------------------------------- failure handling --
