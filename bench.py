@@ -162,7 +162,7 @@ def main():
     ap.add_argument("--n", type=int, default=10**7, help="trajectories per GPU")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=24576)
+    ap.add_argument("--cpu-sample", type=int, default=98304)
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--no-gather", action="store_true", help="skip the NCCL gather of final states (N>1)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -58,6 +58,8 @@ def lib() -> ctypes.CDLL:
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_pi.argtypes = [i32, i32, dbl, dbl, ctypes.POINTER(dbl)]
         L.orc_pi.restype = dbl
+        L.orc_pw.argtypes = [i32, dbl, dbl]
+        L.orc_pw.restype = dbl
         L.orc_error_q.argtypes = [i32, vp, vp, vp, dbl, dbl]
         L.orc_error_q.restype = dbl
         L.orc_uniforms.argtypes = [i32, vp, vp]
@@ -129,6 +131,11 @@ def pi_step(alg: str, accept: bool, h: float, q: float, q_old: float):
     qo = ctypes.c_double(q_old)
     hn = lib().orc_pi(ALGS[alg], int(accept), h, q, ctypes.byref(qo))
     return hn, qo.value
+
+
+def pw(x: float, y: float, dtype="f64") -> float:
+    """The controller's power function x^y (DESIGN R2 polynomial form)."""
+    return lib().orc_pw(DTYPES[dtype], float(x), float(y))
 
 
 def error_q(E, u, unew, abstol, reltol):

@@ -328,6 +328,44 @@ static T error_q(int n, const T* E, const T* u, const T* unew, T abstol, T relto
   return q;
 }
 
+// Controller power function (DESIGN R2 / §4): pw(x, y) = 2^(y·L(x)) with x
+// clamped to [1e-30, 1e30], L(x) = e + s·Σ_k c_k s^{2k} (x = m·2^e, m ∈
+// [√½, √2), s = (m−1)/(m+1), c_k = 2/((2k+1) ln 2)) and 2^z = 2^n·Σ_k
+// (ln 2)^k f^k / k! (n = rint(z), f = z − n). Only exact IEEE operations
+// (frexp, ldexp, rint, +, ×, ÷, fma), so it rounds identically everywhere;
+// accuracy (≈1e-7 fp32, ≈1e-13 fp64 relative) is immaterial to a step-size
+// controller, bitwise reproducibility of accept/reject decisions is not.
+template <class T> struct PwDeg;
+template <> struct PwDeg<float> { static constexpr int L = 4, E = 7; };
+template <> struct PwDeg<double> { static constexpr int L = 8, E = 12; };
+
+template <class T> static T log2_spec(T x) {
+  const double LN2 = 0.693147180559945309417232121458176568;
+  int e;
+  T m = std::frexp(x, &e);                       // x = m·2^e, m ∈ [0.5, 1)
+  if (m < (T)0.70710678118654752440) { m = m * T(2); e -= 1; }
+  const T s = (m - T(1)) / (m + T(1));
+  const T s2 = s * s;
+  T acc = (T)(2.0 / ((2 * PwDeg<T>::L + 1) * LN2));
+  for (int k = PwDeg<T>::L - 1; k >= 0; --k) acc = std::fma(s2, acc, (T)(2.0 / ((2 * k + 1) * LN2)));
+  return std::fma(s, acc, (T)e);
+}
+template <class T> static T exp2_spec(T z) {
+  const double LN2 = 0.693147180559945309417232121458176568;
+  const T nn = std::nearbyint(z);
+  const T f = z - nn;
+  double c[16];
+  c[0] = 1.0;
+  for (int k = 1; k <= PwDeg<T>::E; ++k) c[k] = c[k - 1] * LN2 / k;   // (ln 2)^k / k!, in fp64
+  T acc = (T)c[PwDeg<T>::E];
+  for (int k = PwDeg<T>::E - 1; k >= 0; --k) acc = std::fma(f, acc, (T)c[k]);
+  return std::ldexp(acc, (int)nn);
+}
+template <class T> static T pw(T x, T y) {
+  const T xc = std::fmin(std::fmax(x, (T)1e-30), (T)1e30);
+  return exp2_spec<T>(y * log2_spec<T>(xc));
+}
+
 // Store helpers: save buffer is [k][n] for one trajectory.
 template <class T> static void put(T* save, int n, int j, const T* v) {
   for (int c = 0; c < n; ++c) save[j * n + c] = v[c];
@@ -335,14 +373,14 @@ template <class T> static void put(T* save, int n, int j, const T* v) {
 
 // PI controller (DESIGN R2). Returns the new h after an accepted step.
 template <class T> static T pi_accept(const Ctrl& C, T h, T q, T* q_old) {
-  const T q11 = std::pow(q, (T)C.beta1);
-  T qq = q11 / std::pow(*q_old, (T)C.beta2);
+  const T q11 = pw<T>(q, (T)C.beta1);
+  T qq = q11 / pw<T>(*q_old, (T)C.beta2);
   qq = std::fmax((T)C.qmax_inv, std::fmin((T)C.qmin_inv, qq / (T)C.eta));
   *q_old = std::fmax(q, (T)C.qold_floor);
   return h / qq;
 }
 template <class T> static T pi_reject(const Ctrl& C, T h, T q) {
-  return h / std::fmin((T)C.qmin_inv, std::pow(q, (T)C.beta1) / (T)C.eta);
+  return h / std::fmin((T)C.qmin_inv, pw<T>(q, (T)C.beta1) / (T)C.eta);
 }
 
 template <class T>
@@ -720,6 +758,10 @@ void orc_controller(int alg, double* out6) {
 double orc_pi(int alg, int accept, double h, double q, double* q_old) {
   const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
   return accept ? orc::pi_accept<double>(C, h, q, q_old) : orc::pi_reject<double>(C, h, q);
+}
+// The controller's power function, exported for its pin (vs the libm pow).
+double orc_pw(int dtype, double x, double y) {
+  return dtype == 0 ? (double)orc::pw<float>((float)x, (float)y) : orc::pw<double>(x, y);
 }
 double orc_error_q(int n, const double* E, const double* u, const double* unew, double abstol, double reltol) {
   return orc::error_q<double>(n, E, u, unew, abstol, reltol);

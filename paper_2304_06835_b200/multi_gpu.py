@@ -61,9 +61,9 @@ def shard_weak(n_per_rank: int, rank: int, world: int) -> Shard:
 def allgather_stats(local: torch.Tensor, group=None) -> torch.Tensor:
     """[k, n, 3] per-rank (count, mean, M2) → [R, k, n, 3] on every rank."""
     R = dist.get_world_size(group)
-    out = torch.empty((R, *local.shape), dtype=local.dtype, device=local.device)
+    out = torch.empty((R * local.shape[0], *local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
-    return out
+    return out.view(R, *local.shape)
 
 
 def merge_stats(gathered: torch.Tensor) -> torch.Tensor:

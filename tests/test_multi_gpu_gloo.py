@@ -1,0 +1,85 @@
+"""Host-side multi-rank logic on CPU with gloo, world_size 2 (-m "not gpu").
+
+Covers the sharding maps (every global trajectory exactly once, inputs of a
+shard = the slice of the global inputs), and the two exchange steps of
+paper_2304_06835_b200.multi_gpu (all-gather of statistics triples, gather of
+states to rank 0). The merge itself is a CUDA kernel tested on the GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2304_06835_b200 import multi_gpu as mg
+from synth.inputs import make_inputs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # statistics exchange: rank r contributes triples filled with r
+        local = torch.full((2, 3, 3), float(rank + 1), dtype=torch.float64)
+        g = mg.allgather_stats(local)
+        assert g.shape == (world, 2, 3, 3)
+        for r in range(world):
+            assert torch.all(g[r] == r + 1)
+        # state gather to rank 0
+        st = torch.arange(12, dtype=torch.float32).reshape(3, 4) + 100 * rank
+        out = mg.gather_states(st, dst=0)
+        if rank == 0:
+            assert out.shape == (world, 3, 4)
+            for r in range(world):
+                assert torch.equal(out[r], torch.arange(12, dtype=torch.float32).reshape(3, 4) + 100 * r)
+        else:
+            assert out is None
+        # each rank's shard inputs equal the slice of the global ensemble
+        N_total = 2 * 4096
+        for sh in [mg.shard_contiguous(N_total, rank, world), mg.shard_block_cyclic(N_total, rank, world, chunk=512)]:
+            u0, p = make_inputs("lorenz", "random10", sh.n_local, seed=0xC5, index_offset=sh.index_offset,
+                                chunk_len=sh.chunk_len, chunk_stride=sh.chunk_stride)
+            ug, pg = make_inputs("lorenz", "random10", N_total, seed=0xC5)
+            gi = sh.global_indices().numpy()
+            assert np.array_equal(p, pg[:, gi]) and np.array_equal(u0, ug[:, gi])
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_exchange_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
+@pytest.mark.parametrize("N,R", [(10**8, 8), (10**7 + 3, 4), (5, 2), (1 << 20, 8)])
+def test_shards_cover_every_index_once(N, R):
+    for maker in [mg.shard_contiguous, lambda n, r, w: mg.shard_block_cyclic(n, r, w, chunk=1 << 16)]:
+        shards = [maker(N, r, R) for r in range(R)]
+        assert sum(s.n_local for s in shards) == N
+        if N <= 1 << 20:
+            allidx = np.concatenate([s.global_indices().numpy() for s in shards])
+            assert np.array_equal(np.sort(allidx), np.arange(N))
+    w = [mg.shard_weak(1000, r, 4) for r in range(4)]
+    assert [s.index_offset for s in w] == [0, 1000, 2000, 3000]

@@ -263,6 +263,26 @@ def test_error_proportion_and_pi_controller():
     assert oracle.controller("tsit5")["beta1"] == 7 / 50 and oracle.controller("rosenbrock23")["beta1"] == 7 / 20
 
 
+@pytest.mark.parametrize("dtype,tol", [("f32", 2e-6), ("f64", 1e-12)])
+def test_controller_power_function(dtype, tol):
+    """DESIGN R2: the controller's x^y is a fixed polynomial 2^(y·log2 x); pinned
+    to the math library's pow over the range the controller sees, and to its
+    clamps (x ∈ [1e-30, 1e30])."""
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([10.0 ** rng.uniform(-29, 29, 400), [1e-4, 0.5, 1.0, 1.5, 2.0, 0.7071, 1.4142, 1e-12]])
+    for y in [0.14, 0.08, 0.35, 0.2, -0.14, 1.0]:
+        for x in xs:
+            xt = float(np.float32(x)) if dtype == "f32" else x
+            yt = float(np.float32(y)) if dtype == "f32" else y
+            ref = xt ** yt
+            # rounding of z = y·log2(x) in T dominates for large |z|: bound ∝ (1 + |z|)
+            z = abs(yt * math.log2(xt))
+            assert abs(oracle.pw(xt, yt, dtype) - ref) <= tol * (1 + z) * ref, (x, y)
+    assert oracle.pw(1.0, 0.14, dtype) == 1.0                    # exact at x = 1
+    assert oracle.pw(0.0, 0.14, dtype) == pytest.approx(1e-30 ** 0.14, rel=1e-5)
+    assert oracle.pw(np.inf, 0.14, dtype) == pytest.approx(1e30 ** 0.14, rel=1e-5)
+
+
 # ------------------------------------------------------------------------ LU --
 def test_lu_examples_and_brute_force():
     """P:253-265 LU + substitution: SPEC examples S:136-147, Cramer's rule on random systems."""
