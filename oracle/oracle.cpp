@@ -271,19 +271,19 @@ struct Opts {
 
 // ---------------------------------------------------------------- Tsit5 ----
 // One Tsit5 step from (t,u,k1) with step h:
-//   y_i = u + h Σ_{j<i} a_ij k_j,  k_i = f(y_i, t + c_i h)   (i = 2..7)
+//   y_i = u + Σ_{j<i} (h a_ij) k_j,  k_i = f(y_i, t + c_i h)   (i = 2..7)
 //   u_{n+1} = y_7 (FSAL: b = a_7·), k7 = f(u_{n+1}) = next k1
 //   E = h Σ b̃_i k_i (b̃ = b − b̂)
-// Canonical order: acc = a_i1 k1; acc = fma(a_ij, k_j, acc);
-// y = fma(h, acc, u).
+// Canonical order (DESIGN R1, §4): the step size multiplies each coefficient,
+// h·a_ij rounded to T; y = u; y = fma(h·a_ij, k_j, y) for j = 1..i−1.
 template <class T>
 static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7][8], T* unew, T* E) {
   T y[8];
   for (int i = 1; i < 7; ++i) {
     for (int j = 0; j < n; ++j) {
-      T acc = (T)TS_A[i][0] * K[0][j];
-      for (int l = 1; l < i; ++l) acc = std::fma((T)TS_A[i][l], K[l][j], acc);
-      y[j] = std::fma(h, acc, u[j]);
+      T acc = u[j];
+      for (int l = 0; l < i; ++l) acc = std::fma(h * (T)TS_A[i][l], K[l][j], acc);
+      y[j] = acc;
     }
     const T ti = t + (T)TS_C[i] * h;
     rhs<T>(model, y, p, ti, K[i]);

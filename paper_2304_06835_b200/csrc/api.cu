@@ -2,6 +2,7 @@
 // workspace layout, dispatch over the template instances <Model, T, alg,
 // adaptive, saveat, scheduler>, launch configuration, host end-to-end pipeline.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -96,8 +97,17 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
   const dim3 g = grid_for<T>(a.N), b(kBlock);
   if (alg == ENS_TSIT5) {
     if (!opt->adaptive) {
-      if (save) tsit5_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
-      else tsit5_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+      if constexpr (std::is_same<T, float>::value) {
+        // fp32: two trajectories per thread on the packed FFMA2 path
+        const auto cf = make_tsit_coef<float, float2>(a.dt0, a.h_last);
+        const dim3 g2((unsigned)cdiv(a.N, 2 * kBlock));
+        if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b, 0, s>>>(a, cf);
+        else tsit5_fixed_kernel<M, f2, false><<<g2, b, 0, s>>>(a, cf);
+      } else {
+        const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
+        if (save) tsit5_fixed_kernel<M, double, true><<<g, b, 0, s>>>(a, cf);
+        else tsit5_fixed_kernel<M, double, false><<<g, b, 0, s>>>(a, cf);
+      }
     } else if (opt->refill) {
       int occ = 0;
       if (save) {

@@ -1,19 +1,24 @@
 // tsit5.cuh — per-thread Tsit5 5(4) integrator for sm_100a.
 //
-// One trajectory per thread (the paper's EnsembleGPUKernel, Listing 1
-// P:287-307). State, the seven stage vectors, the error estimate and the
-// controller live in registers ("stack allocate all intermediates").
-// Tableau coefficients are compile-time immediates; the canonical operation
-// order makes each stage sum
-//     acc = a_i1 k1;  acc = fma(a_ij, k_j, acc) (j = 2..i-1);  y = fma(h, acc, u)
-// which is the paper's u_n + h Σ a_ij k_j (reading R1).
+// One trajectory per lane (the paper's EnsembleGPUKernel, Listing 1
+// P:287-307); the fixed-step fp32 kernel carries TWO trajectories per thread
+// in packed f2 lanes (FFMA2/FADD2/FMUL2), bit-identical per trajectory. State,
+// the seven stage vectors, the error estimate and the controller live in
+// registers ("stack allocate all intermediates").
+//
+// Stage sums (DESIGN R1, §4): y_i = u + Σ_{l<i} (h·a_il) k_l, evaluated
+//     y = u; y = fma(h·a_il, k_l, y)  (l = 1..i−1)
+// with the products h·a_il rounded to T: i−1 FMAs per component and stage.
+// Fixed-step runs take the 21 products from kernel parameters (computed once
+// on the host, uniform registers in SASS); adaptive runs form them per step.
 #pragma once
 #include "common.cuh"
+#include "vec2.cuh"
 
 namespace ens {
 
 // Tsitouras (2011) coefficients, as published (Tsit5). Double literals,
-// converted to T once at compile time (DESIGN R7).
+// converted to T once (DESIGN R7).
 __host__ __device__ constexpr double ts_a(int i, int j) {
   constexpr double A[7][7] = {
       {0, 0, 0, 0, 0, 0, 0},
@@ -48,22 +53,48 @@ __host__ __device__ constexpr double ts_r(int i, int j) {
                               {0.0, 1.5, -4.0, 2.5}};
   return R[i][j];
 }
+// (i, l), 1 ≤ i ≤ 6, l < i  →  0..20
+__host__ __device__ constexpr int ts_idx(int i, int l) { return i * (i - 1) / 2 + l; }
+
+// Step-scaled coefficients h·a_il for the fixed step dt (h) and the last step (hl).
+// C = float, double, or float2 (the same float product broadcast to both lanes).
+template <class C> struct TsitCoef { C h[21]; C hl[21]; };
+template <class V> struct CoefOf { using C = V; };
+template <> struct CoefOf<f2> { using C = float2; };
+__device__ __forceinline__ float coef_to(float c, float*) { return c; }
+__device__ __forceinline__ double coef_to(double c, double*) { return c; }
+__device__ __forceinline__ f2 coef_to(float2 c, f2*) { return f2(c); }
+
+template <class V, class C> struct HaParam {      // coefficients read from kernel parameters
+  const C* p;
+  __device__ __forceinline__ V operator()(int i, int l) const { return coef_to(p[ts_idx(i, l)], (V*)nullptr); }
+};
+template <class V> struct HaReg {                  // coefficients formed in registers for this step
+  V v[21];
+  __device__ __forceinline__ explicit HaReg(V h) {
+#pragma unroll
+    for (int i = 1; i < 7; ++i)
+#pragma unroll
+      for (int l = 0; l < i; ++l) v[ts_idx(i, l)] = h * V(ts_a(i, l));
+  }
+  __device__ __forceinline__ V operator()(int i, int l) const { return v[ts_idx(i, l)]; }
+};
 
 // Stages 2..7 from (t, u, K[0] = f(u)): fills K[1..6] and y = u_{n+1} (= y_7, FSAL).
-template <class M, class T>
-__device__ __forceinline__ void tsit5_stages(const T (&par)[M::m], T t, T h, const T (&u)[M::n], T (&K)[7][M::n],
-                                             T (&y)[M::n]) {
+template <class M, class V, class HA>
+__device__ __forceinline__ void tsit5_stages(const V (&par)[M::m], V t, V h, const HA& ha, const V (&u)[M::n],
+                                             V (&K)[7][M::n], V (&y)[M::n]) {
   constexpr int n = M::n;
 #pragma unroll
   for (int i = 1; i < 7; ++i) {
 #pragma unroll
     for (int j = 0; j < n; ++j) {
-      T acc = T(ts_a(i, 0)) * K[0][j];
+      V acc = u[j];
 #pragma unroll
-      for (int l = 1; l < i; ++l) acc = fmaT(T(ts_a(i, l)), K[l][j], acc);
-      y[j] = fmaT(h, acc, u[j]);
+      for (int l = 0; l < i; ++l) acc = fmaT(ha(i, l), K[l][j], acc);
+      y[j] = acc;
     }
-    M::f(y, par, t + T(ts_c(i)) * h, K[i]);
+    M::f(y, par, t + V(ts_c(i)) * h, K[i]);
   }
 }
 
@@ -80,35 +111,77 @@ __device__ __forceinline__ void tsit5_error(T h, const T (&K)[7][n], T (&E)[n]) 
 }
 
 // u(t + θh) = u + h Σ b_i(θ) k_i
-template <int n, class T>
-__device__ __forceinline__ void tsit5_interp(T theta, T h, const T (&u)[n], const T (&K)[7][n], T (&o)[n]) {
-  T bt[7];
-  bt[0] = fmaT(theta, fmaT(theta, fmaT(theta, T(ts_r(0, 3)), T(ts_r(0, 2))), T(ts_r(0, 1))), T(ts_r(0, 0))) * theta;
-  const T th2 = theta * theta;
+template <int n, class V>
+__device__ __forceinline__ void tsit5_interp(V theta, V h, const V (&u)[n], const V (&K)[7][n], V (&o)[n]) {
+  V bt[7];
+  bt[0] = fmaT(theta, fmaT(theta, fmaT(theta, V(ts_r(0, 3)), V(ts_r(0, 2))), V(ts_r(0, 1))), V(ts_r(0, 0))) * theta;
+  const V th2 = theta * theta;
 #pragma unroll
-  for (int i = 1; i < 7; ++i) bt[i] = fmaT(theta, fmaT(theta, T(ts_r(i, 3)), T(ts_r(i, 2))), T(ts_r(i, 1))) * th2;
+  for (int i = 1; i < 7; ++i) bt[i] = fmaT(theta, fmaT(theta, V(ts_r(i, 3)), V(ts_r(i, 2))), V(ts_r(i, 1))) * th2;
 #pragma unroll
   for (int j = 0; j < n; ++j) {
-    T acc = bt[0] * K[0][j];
+    V acc = bt[0] * K[0][j];
 #pragma unroll
     for (int i = 1; i < 7; ++i) acc = fmaT(bt[i], K[i][j], acc);
     o[j] = fmaT(h, acc, u[j]);
   }
 }
 
-// Save every τ_j ∈ (t, tn] of an accepted step [t, tn] (DESIGN R5).
-template <int n, class T>
-__device__ __forceinline__ void tsit5_save(const Args<T>& a, int64_t i, int& js, T t, T tn, T h, const T (&u)[n],
-                                           const T (&K)[7][n], const T (&un)[n]) {
+// ---------------------------------------------------- lane load / store --
+template <class M, class V, class T>
+__device__ __forceinline__ void load_lanes(const Args<T>& a, const int64_t (&idx)[LaneOf<V>::W], V (&u)[M::n],
+                                           V (&par)[M::m]) {
+  constexpr int W = LaneOf<V>::W;
+#pragma unroll
+  for (int c = 0; c < M::n; ++c) {
+    T x[2];
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] = __ldg(a.u0 + (size_t)c * a.ld + idx[w]);
+    u[c] = make_lanes<V>(x[0], x[W - 1]);
+  }
+#pragma unroll
+  for (int c = 0; c < M::m; ++c) {
+    T x[2];
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] = a.p_broadcast ? __ldg(a.p + c) : __ldg(a.p + (size_t)c * a.ld + idx[w]);
+    par[c] = make_lanes<V>(x[0], x[W - 1]);
+  }
+}
+
+template <int n, class V, class T>
+__device__ __forceinline__ void store_lanes(const Args<T>& a, const int64_t (&idx)[LaneOf<V>::W],
+                                            const bool (&live)[LaneOf<V>::W], int j, const V (&v)[n]) {
+#pragma unroll
+  for (int w = 0; w < LaneOf<V>::W; ++w)
+    if (live[w]) {
+#pragma unroll
+      for (int c = 0; c < n; ++c) a.u_out[((size_t)j * n + c) * a.ld + idx[w]] = lane(v[c], w);
+    }
+}
+
+template <int n, class V>
+__device__ __forceinline__ bool lane_finite(const V (&v)[n], int w) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < n; ++c) ok = ok && finiteT(lane(v[c], w));
+  return ok;
+}
+
+// Save every τ_j ∈ (t, tn] of an accepted step [t, tn] (DESIGN R5). In
+// fixed-step runs t, tn, h are shared by the lanes of a thread.
+template <int n, class V, class T>
+__device__ __forceinline__ void tsit5_save(const Args<T>& a, const int64_t (&idx)[LaneOf<V>::W],
+                                           const bool (&live)[LaneOf<V>::W], int& js, T t, T tn, T h,
+                                           const V (&u)[n], const V (&K)[7][n], const V (&un)[n]) {
   while (js < a.k) {
     const T tau = __ldg(a.tau + js);
     if (!(tau <= tn)) break;
     if (tau == tn) {
-      store_point<n>(a, i, js, un);
+      store_lanes<n, V, T>(a, idx, live, js, un);
     } else {
-      T o[n];
-      tsit5_interp<n, T>((tau - t) / h, h, u, K, o);
-      store_point<n>(a, i, js, o);
+      V o[n];
+      tsit5_interp<n, V>(splat<V>((tau - t) / h), splat<V>(h), u, K, o);
+      store_lanes<n, V, T>(a, idx, live, js, o);
     }
     ++js;
   }
@@ -117,51 +190,77 @@ __device__ __forceinline__ void tsit5_save(const Args<T>& a, int64_t i, int& js,
 // ---------------------------------------------------------------- fixed dt --
 // Fixed grid (DESIGN R3): nsteps steps of dt, the last of h_last. No error
 // estimate. Divergence is checked on f(u0) and the final state (DESIGN R6).
-template <class M, class T, bool SAVE>
-__global__ void __launch_bounds__(256) tsit5_fixed_kernel(const Args<T> a) {
-  constexpr int n = M::n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.N) return;
-  T u[n], par[M::m], K[7][n], y[n];
-  load_column<M, T>(a, i, u, par);
-  M::f(u, par, a.t0, K[0]);
+// V = float2-pair (two trajectories per thread), float or double.
+template <class M, class V, bool SAVE>
+__global__ void __launch_bounds__(256)
+    tsit5_fixed_kernel(const Args<typename LaneOf<V>::T> a, const TsitCoef<typename CoefOf<V>::C> cf) {
+  using T = typename LaneOf<V>::T;
+  using C = typename CoefOf<V>::C;
+  constexpr int n = M::n, W = LaneOf<V>::W;
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
+  if (i0 >= a.N) return;
+  int64_t idx[W];
+  bool live[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) { idx[w] = min(i0 + w, a.N - 1); live[w] = (i0 + w < a.N); }
+  V u[n], par[M::m], K[7][n], y[n];
+  load_lanes<M, V, T>(a, idx, u, par);
+  M::f(u, par, splat<V>(a.t0), K[0]);
   int js = 0;
   if (SAVE) {
-    while (js < a.k && __ldg(a.tau + js) <= a.t0) { store_point<n>(a, i, js, u); ++js; }
+    while (js < a.k && __ldg(a.tau + js) <= a.t0) { store_lanes<n, V, T>(a, idx, live, js, u); ++js; }
   }
-  int32_t ret = RET_SUCCESS;
-  int64_t steps = a.nsteps;
-  if (!all_finite<n>(K[0])) { ret = RET_DIVERGED; steps = 0; }
-  const T hdt = a.dt0;
+  const int64_t steps = a.nsteps;
+  // a lane whose f(u0) is non-finite is finished now (Diverged, no step taken)
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    if (live[w] && !lane_finite<n, V>(K[0], w)) {
+      for (int j = js; j < (SAVE ? a.k : 1); ++j)
+#pragma unroll
+        for (int c = 0; c < n; ++c)
+          a.u_out[((size_t)j * n + c) * a.ld + idx[w]] = SAVE ? nanT<T>() : lane(u[c], w);
+      if (a.retcode) a.retcode[idx[w]] = RET_DIVERGED;
+      if (a.nacc) a.nacc[idx[w]] = 0;
+      if (a.nrej) a.nrej[idx[w]] = 0;
+      live[w] = false;
+    }
+  }
+  bool any = false;
+#pragma unroll
+  for (int w = 0; w < W; ++w) any = any || live[w];
+  if (!any) return;
+  const V hdt = splat<V>(a.dt0);
+  const HaParam<V, C> ha{cf.h};
   // all steps but the last: constant h (no per-step select in the hot loop)
   for (int64_t s = 0; s + 1 < steps; ++s) {
     T t = T(0);
     if (SAVE) t = (T)(a.t0d + (double)s * a.dtd);
-    tsit5_stages<M, T>(par, t, hdt, u, K, y);
-    if (SAVE) tsit5_save<n, T>(a, i, js, t, (T)(a.t0d + (double)(s + 1) * a.dtd), hdt, u, K, y);
+    tsit5_stages<M, V>(par, splat<V>(t), hdt, ha, u, K, y);
+    if (SAVE) tsit5_save<n, V, T>(a, idx, live, js, t, (T)(a.t0d + (double)(s + 1) * a.dtd), a.dt0, u, K, y);
 #pragma unroll
     for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
   }
-  if (steps > 0) {   // last step: h_last, lands on tf exactly
-    const int64_t s = steps - 1;
-    const T t = (T)(a.t0d + (double)s * a.dtd);
-    tsit5_stages<M, T>(par, t, a.h_last, u, K, y);
-    if (SAVE) tsit5_save<n, T>(a, i, js, t, a.tf, a.h_last, u, K, y);
-#pragma unroll
-    for (int j = 0; j < n; ++j) u[j] = y[j];
-    if (!all_finite<n>(u)) ret = RET_DIVERGED;
+  {   // last step: h_last, lands on tf exactly
+    const T t = (T)(a.t0d + (double)(steps - 1) * a.dtd);
+    const HaParam<V, C> hal{cf.hl};
+    tsit5_stages<M, V>(par, splat<V>(t), splat<V>(a.h_last), hal, u, K, y);
+    if (SAVE) tsit5_save<n, V, T>(a, idx, live, js, t, a.tf, a.h_last, u, K, y);
   }
   if (SAVE) {
-    T nanv[n];
+    V nanv[n];
 #pragma unroll
-    for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
-    for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
+    for (int j = 0; j < n; ++j) nanv[j] = splat<V>(nanT<T>());
+    for (; js < a.k; ++js) store_lanes<n, V, T>(a, idx, live, js, nanv);
   } else {
-    store_point<n>(a, i, 0, u);
+    store_lanes<n, V, T>(a, idx, live, 0, y);
   }
-  if (a.retcode) a.retcode[i] = ret;
-  if (a.nacc) a.nacc[i] = (int32_t)steps;
-  if (a.nrej) a.nrej[i] = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (live[w]) {
+      if (a.retcode) a.retcode[idx[w]] = lane_finite<n, V>(y, w) ? RET_SUCCESS : RET_DIVERGED;
+      if (a.nacc) a.nacc[idx[w]] = (int32_t)steps;
+      if (a.nrej) a.nrej[idx[w]] = 0;
+    }
 }
 
 // ----------------------------------------------------------------- adaptive --
@@ -196,13 +295,18 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     const bool last = (t + h >= a.tf);
     if (last) h = a.tf - t;
     T y[n], E[n];
-    tsit5_stages<M, T>(par, t, h, u, K, y);
+    const HaReg<T> ha(h);
+    tsit5_stages<M, T>(par, t, h, ha, u, K, y);
     tsit5_error<n, T>(h, K, E);
     const T q = error_q<n, T>(E, u, y, a.abstol, a.reltol);
     ++attempts;
     if (q < T(1)) {
       const T tn = last ? a.tf : t + h;
-      if (SAVE) tsit5_save<n, T>(a, i, js, t, tn, h, u, K, y);
+      if (SAVE) {
+        const int64_t id[1] = {i};
+        const bool lv[1] = {true};
+        tsit5_save<n, T, T>(a, id, lv, js, t, tn, h, u, K, y);
+      }
       t = tn;
 #pragma unroll
       for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
@@ -230,5 +334,24 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     if (a.nrej) a.nrej[i] = nrej;
   }
 };
+
+// Host-side construction of the fixed-step coefficient table (products in T).
+template <class T, class C>
+inline TsitCoef<C> make_tsit_coef(T h, T hl) {
+  TsitCoef<C> cf;
+  for (int i = 1; i < 7; ++i)
+    for (int l = 0; l < i; ++l) {
+      const T a = (T)ts_a(i, l);
+      const T x = h * a, y = hl * a;
+      if constexpr (sizeof(C) == 2 * sizeof(T)) {
+        cf.h[ts_idx(i, l)] = C{x, x};
+        cf.hl[ts_idx(i, l)] = C{y, y};
+      } else {
+        cf.h[ts_idx(i, l)] = x;
+        cf.hl[ts_idx(i, l)] = y;
+      }
+    }
+  return cf;
+}
 
 }  // namespace ens

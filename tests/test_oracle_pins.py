@@ -99,7 +99,7 @@ def test_tsit5_expdecay_closed_form():
     assert abs(_R_tsit5(-0.1, 1 / 720) ** 10 - v) > 1e-13
     # several λ, h (vectorised over trajectories) in fp64 and fp32
     lam = np.array([0.5, 1.0, 3.0, 7.5])
-    for dtype, tol in [("f64", 1e-13), ("f32", 2e-6)]:
+    for dtype, tol in [("f64", 1e-13), ("f32", 1e-5)]:   # fp32: 40 steps × a few ulp
         out, rc, na, _ = oracle.solve("expdecay", "tsit5", np.ones((1, 4)), lam[None, :], (0, 2), 0.05, dtype=dtype)
         expect = _R_tsit5(-lam * 0.05, g6) ** 40
         np.testing.assert_allclose(out[0, 0].astype(np.float64), expect, rtol=tol)
