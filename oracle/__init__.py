@@ -58,10 +58,12 @@ def lib() -> ctypes.CDLL:
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_pi.argtypes = [i32, i32, dbl, dbl, ctypes.POINTER(dbl)]
         L.orc_pi.restype = dbl
-        L.orc_pw.argtypes = [i32, dbl, dbl]
-        L.orc_pw.restype = dbl
-        L.orc_error_q.argtypes = [i32, vp, vp, vp, dbl, dbl]
-        L.orc_error_q.restype = dbl
+        L.orc_log2.argtypes = [i32, dbl]
+        L.orc_log2.restype = dbl
+        L.orc_exp2.argtypes = [i32, dbl]
+        L.orc_exp2.restype = dbl
+        L.orc_error_q2.argtypes = [i32, vp, vp, vp, dbl, dbl]
+        L.orc_error_q2.restype = dbl
         L.orc_uniforms.argtypes = [i32, vp, vp]
         L.orc_normals.argtypes = [i32, u64, u64, i64, i64, vp]
         L.orc_fixed_grid.argtypes = [dbl, dbl, dbl, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
@@ -126,22 +128,26 @@ def controller(alg: str):
     return dict(zip(["beta1", "beta2", "eta", "qmin_inv", "qmax_inv", "qold_floor"], out.tolist()))
 
 
-def pi_step(alg: str, accept: bool, h: float, q: float, q_old: float):
-    """PI controller (fp64): returns (h_new, q_old_new)."""
-    qo = ctypes.c_double(q_old)
-    hn = lib().orc_pi(ALGS[alg], int(accept), h, q, ctypes.byref(qo))
-    return hn, qo.value
+def pi_step(alg: str, accept: bool, h: float, q2: float, lq_old: float):
+    """PI controller (fp64, exponent domain, DESIGN R2): returns (h_new, log2 q_old after the step)."""
+    lo = ctypes.c_double(lq_old)
+    hn = lib().orc_pi(ALGS[alg], int(accept), h, q2, ctypes.byref(lo))
+    return hn, lo.value
 
 
-def pw(x: float, y: float, dtype="f64") -> float:
-    """The controller's power function x^y (DESIGN R2 polynomial form)."""
-    return lib().orc_pw(DTYPES[dtype], float(x), float(y))
+def log2_spec(x: float, dtype="f64") -> float:
+    return lib().orc_log2(DTYPES[dtype], float(x))
 
 
-def error_q(E, u, unew, abstol, reltol):
+def exp2_spec(z: float, dtype="f64") -> float:
+    return lib().orc_exp2(DTYPES[dtype], float(z))
+
+
+def error_q2(E, u, unew, abstol, reltol):
+    """Squared error proportion q² (Eq. q, RMS reading)."""
     E = np.ascontiguousarray(E, np.float64); u = np.ascontiguousarray(u, np.float64)
     un = np.ascontiguousarray(unew, np.float64)
-    return lib().orc_error_q(E.size, _p(E), _p(u), _p(un), abstol, reltol)
+    return lib().orc_error_q2(E.size, _p(E), _p(u), _p(un), abstol, reltol)
 
 
 def philox(ctr, key):

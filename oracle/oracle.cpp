@@ -314,27 +314,28 @@ static void tsit5_interp(int n, T theta, T h, const T* u, T K[7][8], T* out) {
   }
 }
 
-// Error proportion q (P:117-119 Eq. q), RMS norm (DESIGN R4), component-wise max.
+// Squared error proportion q² (P:117-119 Eq. q), RMS norm (DESIGN R4),
+// component-wise max{|u(t)|, |u(t+h)|}. Accept iff q² < 1 (⟺ q < 1).
+// Non-finite → +∞.
 template <class T>
-static T error_q(int n, const T* E, const T* u, const T* unew, T abstol, T reltol) {
+static T error_q2(int n, const T* E, const T* u, const T* unew, T abstol, T reltol) {
   T s = T(0);
   for (int j = 0; j < n; ++j) {
     const T sc = abstol + reltol * std::fmax(std::fabs(u[j]), std::fabs(unew[j]));
     const T r = E[j] / sc;
     s = (j == 0) ? r * r : std::fma(r, r, s);
   }
-  T q = std::sqrt(s / (T)n);
-  if (!std::isfinite(q)) q = std::numeric_limits<T>::infinity();
-  return q;
+  T q2 = s * (T)(1.0 / n);
+  if (!std::isfinite(q2)) q2 = std::numeric_limits<T>::infinity();
+  return q2;
 }
 
-// Controller power function (DESIGN R2 / §4): pw(x, y) = 2^(y·L(x)) with x
-// clamped to [1e-30, 1e30], L(x) = e + s·Σ_k c_k s^{2k} (x = m·2^e, m ∈
-// [√½, √2), s = (m−1)/(m+1), c_k = 2/((2k+1) ln 2)) and 2^z = 2^n·Σ_k
-// (ln 2)^k f^k / k! (n = rint(z), f = z − n). Only exact IEEE operations
-// (frexp, ldexp, rint, +, ×, ÷, fma), so it rounds identically everywhere;
-// accuracy (≈1e-7 fp32, ≈1e-13 fp64 relative) is immaterial to a step-size
-// controller, bitwise reproducibility of accept/reject decisions is not.
+// log2 and exp2 for the step-size controller (DESIGN R2 / §4):
+// L(x) = e + s·Σ_k c_k s^{2k}   (x = m·2^e, m ∈ [√½, √2), s = (m−1)/(m+1), c_k = 2/((2k+1) ln 2)),
+// 2^z  = 2^n·Σ_k (ln 2)^k f^k / k!   (n = rint(z), f = z − n).
+// Only exact IEEE operations (frexp, ldexp, rint, +, ×, ÷, fma), so they round
+// identically on every implementation (libm and CUDA pow/log2 differ in the last
+// ulp, which flips accept/reject decisions); accuracy ≈1e-7 (fp32) / 1e-13 (fp64).
 template <class T> struct PwDeg;
 template <> struct PwDeg<float> { static constexpr int L = 4, E = 7; };
 template <> struct PwDeg<double> { static constexpr int L = 8, E = 12; };
@@ -361,26 +362,39 @@ template <class T> static T exp2_spec(T z) {
   for (int k = PwDeg<T>::E - 1; k >= 0; --k) acc = std::fma(f, acc, (T)c[k]);
   return std::ldexp(acc, (int)nn);
 }
-template <class T> static T pw(T x, T y) {
-  const T xc = std::fmin(std::fmax(x, (T)1e-30), (T)1e30);
-  return exp2_spec<T>(y * log2_spec<T>(xc));
-}
 
 // Store helpers: save buffer is [k][n] for one trajectory.
 template <class T> static void put(T* save, int n, int j, const T* v) {
   for (int c = 0; c < n; ++c) save[j * n + c] = v[c];
 }
 
-// PI controller (DESIGN R2). Returns the new h after an accepted step.
-template <class T> static T pi_accept(const Ctrl& C, T h, T q, T* q_old) {
-  const T q11 = pw<T>(q, (T)C.beta1);
-  T qq = q11 / pw<T>(*q_old, (T)C.beta2);
-  qq = std::fmax((T)C.qmax_inv, std::fmin((T)C.qmin_inv, qq / (T)C.eta));
-  *q_old = std::fmax(q, (T)C.qold_floor);
-  return h / qq;
+// PI controller (P:120 h_new = η q_{n−1}^{β2} q_n^{β1} h; DESIGN R2) in the
+// exponent domain. With Lq = log2 q = ½·L(q²) (q² clamped to [1e-30, 1e30]) and
+// Lold = log2 q_old, the factor η·q^{−β1}·q_old^{β2}, clamped to [1/5, 10], is 2^{−z}:
+//   accept: z = clamp(β1·Lq − β2·Lold + log2(1/η), log2 0.1, log2 5);  Lold ← max(Lq, log2 1e-4)
+//   reject: z = min(β1·Lq + log2(1/η), log2 5)
+//   h_new = h·2^{−z}
+static const double C_ETA = 0.15200309344505006;     // log2(1/0.9)
+static const double Z_MIN = -3.321928094887362;       // log2(0.1)
+static const double Z_MAX = 2.321928094887362;        // log2(5)
+static const double L_FLOOR = -13.287712379549449;    // log2(1e-4)
+
+template <class T> static T half_log2_q(T q2) {
+  const T x = std::fmin(std::fmax(q2, (T)1e-30), (T)1e30);
+  return T(0.5) * log2_spec<T>(x);
 }
-template <class T> static T pi_reject(const Ctrl& C, T h, T q) {
-  return h / std::fmin((T)C.qmin_inv, pw<T>(q, (T)C.beta1) / (T)C.eta);
+template <class T> static T pi_accept(const Ctrl& C, T h, T q2, T* lq_old) {
+  const T lq = half_log2_q<T>(q2);
+  T z = std::fma((T)C.beta1, lq, (T)C_ETA);
+  z = std::fma(-(T)C.beta2, *lq_old, z);
+  z = std::fmin((T)Z_MAX, std::fmax((T)Z_MIN, z));
+  *lq_old = std::fmax(lq, (T)L_FLOOR);
+  return h * exp2_spec<T>(-z);
+}
+template <class T> static T pi_reject(const Ctrl& C, T h, T q2) {
+  const T lq = half_log2_q<T>(q2);
+  const T z = std::fmin((T)Z_MAX, std::fma((T)C.beta1, lq, (T)C_ETA));
+  return h * exp2_spec<T>(-z);
 }
 
 template <class T>
@@ -426,16 +440,16 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
     const Ctrl& C = CTRL_TSIT5;
     const T abstol = (T)o.abstol, reltol = (T)o.reltol;
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T q_old = (T)C.qold_floor;
+    T lq_old = (T)L_FLOOR;
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
       const bool last = (t + h >= tf);
       if (last) h = tf - t;
       tsit5_step<T>(model, n, p, t, h, u, K, unew, E);
-      const T q = error_q<T>(n, E, u, unew, abstol, reltol);
+      const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
-      if (q < T(1)) {                              // accept iff q < 1
+      if (q2 < T(1)) {                              // accept iff q < 1
         const T tn = last ? tf : t + h;
         while (js < k && tau[js] <= tn) {
           if (tau[js] == tn) put(tr.save, n, js, unew);
@@ -445,9 +459,9 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
         t = tn;
         for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
         tr.n_accept++;
-        h = pi_accept<T>(C, h, q, &q_old);
+        h = pi_accept<T>(C, h, q2, &lq_old);
       } else {
-        h = pi_reject<T>(C, h, q);
+        h = pi_reject<T>(C, h, q2);
         tr.n_reject++;
       }
       if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
@@ -532,7 +546,7 @@ static bool ros23_step(int model, int n, const T* p, T t, T h, const T* u, const
     rhsv[j] = std::fma(T(-2), k1[j] - F0[j], a);
   }
   lu_solve<T>(n, W, piv, inv, rhsv, k3);                                // k3
-  const T h6 = h / T(6);
+  const T h6 = h * (T)(1.0 / 6.0);
   for (int j = 0; j < n; ++j) {                                         // E = h/6 (k1 − 2 k2 + k3)
     const T s = std::fma(T(-2), k2[j], k1[j]) + k3[j];
     E[j] = h6 * s;
@@ -595,7 +609,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
     if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
   } else {
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T q_old = (T)C.qold_floor;
+    T lq_old = (T)L_FLOOR;
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -608,8 +622,8 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
         if (t + h == t) { tr.retcode = RET_SINGULAR; break; }
         continue;
       }
-      const T q = error_q<T>(n, E, u, unew, abstol, reltol);
-      if (q < T(1)) {
+      const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
+      if (q2 < T(1)) {
         const T tn = last ? tf : t + h;
         while (js < k && tau[js] <= tn) {
           if (tau[js] == tn) put(tr.save, n, js, unew);
@@ -619,9 +633,9 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
         t = tn;
         for (int j = 0; j < n; ++j) { u[j] = unew[j]; F0[j] = F2[j]; }
         tr.n_accept++;
-        h = pi_accept<T>(C, h, q, &q_old);
+        h = pi_accept<T>(C, h, q2, &lq_old);
       } else {
-        h = pi_reject<T>(C, h, q);
+        h = pi_reject<T>(C, h, q2);
         tr.n_reject++;
       }
       if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
@@ -754,17 +768,19 @@ void orc_controller(int alg, double* out6) {
   out6[5] = C.qold_floor;
 }
 
-// Controller / error-norm pins (fp64): returns h_new; *q_old updated on accept.
-double orc_pi(int alg, int accept, double h, double q, double* q_old) {
+// Controller / error-norm pins (fp64): returns h_new; *lq_old (= log2 q_old) updated on accept.
+double orc_pi(int alg, int accept, double h, double q2, double* lq_old) {
   const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
-  return accept ? orc::pi_accept<double>(C, h, q, q_old) : orc::pi_reject<double>(C, h, q);
+  return accept ? orc::pi_accept<double>(C, h, q2, lq_old) : orc::pi_reject<double>(C, h, q2);
 }
-// The controller's power function, exported for its pin (vs the libm pow).
-double orc_pw(int dtype, double x, double y) {
-  return dtype == 0 ? (double)orc::pw<float>((float)x, (float)y) : orc::pw<double>(x, y);
+double orc_log2(int dtype, double x) {
+  return dtype == 0 ? (double)orc::log2_spec<float>((float)x) : orc::log2_spec<double>(x);
 }
-double orc_error_q(int n, const double* E, const double* u, const double* unew, double abstol, double reltol) {
-  return orc::error_q<double>(n, E, u, unew, abstol, reltol);
+double orc_exp2(int dtype, double z) {
+  return dtype == 0 ? (double)orc::exp2_spec<float>((float)z) : orc::exp2_spec<double>(z);
+}
+double orc_error_q2(int n, const double* E, const double* u, const double* unew, double abstol, double reltol) {
+  return orc::error_q2<double>(n, E, u, unew, abstol, reltol);
 }
 
 void orc_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {

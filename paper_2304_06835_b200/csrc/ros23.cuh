@@ -124,7 +124,7 @@ __device__ __forceinline__ bool ros23_step(const T (&par)[M::m], T t, T h, const
     r[j] = fmaT(T(-2), k1[j] - F0[j], aa);   // F2 − e32(k2 − F1) − 2(k1 − F0)
   }
   lu_solve<n, T>(W, piv, inv, r, k3);
-  const T h6 = h / T(6);
+  const T h6 = h * T(1.0 / 6.0);
 #pragma unroll
   for (int j = 0; j < n; ++j) E[j] = h6 * (fmaT(T(-2), k2[j], k1[j]) + k3[j]);   // E = h/6 (k1 − 2k2 + k3)
   return ok;
@@ -160,14 +160,14 @@ __device__ __forceinline__ void ros23_save(const Args<T>& a, int64_t i, int& js,
 template <class M, class T, bool SAVE> struct Ros23Lane {
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
-  T t, h, q_old;
+  T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret, js;
   int64_t attempts;
   bool done;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
-    t = a.t0; h = a.dt0; q_old = T(1e-4);
+    t = a.t0; h = a.dt0; lq_old = T(kLFloor);
     nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
     M::f(u, par, t, F0);
     if (SAVE) {
@@ -189,17 +189,17 @@ template <class M, class T, bool SAVE> struct Ros23Lane {
       if (t + h == t) { ret = RET_SINGULAR; done = true; }
       return;
     }
-    const T q = error_q<n, T>(E, u, un, a.abstol, a.reltol);
-    if (q < T(1)) {
+    const T q2 = error_q2<n, T>(E, u, un, a.abstol, a.reltol);
+    if (q2 < T(1)) {
       const T tn = last ? a.tf : t + h;
       if (SAVE) ros23_save<n, T>(a, i, js, t, tn, h, u, k1, k2, un);
       t = tn;
 #pragma unroll
       for (int j = 0; j < n; ++j) { u[j] = un[j]; F0[j] = F2[j]; }
       ++nacc;
-      h = pi_accept<T>(h, q, q_old, 7.0 / 20.0, 2.0 / 10.0);
+      h = pi_accept<T>(h, q2, lq_old, 7.0 / 20.0, 2.0 / 10.0);
     } else {
-      h = pi_reject<T>(h, q, 7.0 / 20.0);
+      h = pi_reject<T>(h, q2, 7.0 / 20.0);
       ++nrej;
     }
     if (!(t < a.tf)) done = true;

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256)
 template <class M, class T, bool SAVE> struct Tsit5Lane {
   static constexpr int n = M::n;
   T u[n], par[M::m], K[7][n];
-  T t, h, q_old;
+  T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret;
   int32_t js;
   int64_t attempts;
@@ -279,7 +279,7 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     load_column<M, T>(a, i, u, par);
     t = a.t0;
     h = a.dt0;                 // (T)min(dt, tf − t0), computed on the host in fp64
-    q_old = T(1e-4);
+    lq_old = T(kLFloor);
     nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
     M::f(u, par, t, K[0]);
     if (SAVE) {
@@ -298,9 +298,9 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     const HaReg<T> ha(h);
     tsit5_stages<M, T>(par, t, h, ha, u, K, y);
     tsit5_error<n, T>(h, K, E);
-    const T q = error_q<n, T>(E, u, y, a.abstol, a.reltol);
+    const T q2 = error_q2<n, T>(E, u, y, a.abstol, a.reltol);
     ++attempts;
-    if (q < T(1)) {
+    if (q2 < T(1)) {
       const T tn = last ? a.tf : t + h;
       if (SAVE) {
         const int64_t id[1] = {i};
@@ -311,9 +311,9 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
 #pragma unroll
       for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
       ++nacc;
-      h = pi_accept<T>(h, q, q_old, 7.0 / 50.0, 2.0 / 25.0);
+      h = pi_accept<T>(h, q2, lq_old, 7.0 / 50.0, 2.0 / 25.0);
     } else {
-      h = pi_reject<T>(h, q, 7.0 / 50.0);
+      h = pi_reject<T>(h, q2, 7.0 / 50.0);
       ++nrej;
     }
     if (!(t < a.tf)) done = true;

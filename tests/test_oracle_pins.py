@@ -235,52 +235,55 @@ def test_sde_diffusion_definitions():
 
 
 # --------------------------------------------------------------- controller --
+L_FLOOR = math.log2(1e-4)
+
+
 def test_error_proportion_and_pi_controller():
-    """Eq. q (P:117-119) RMS reading: S:248 example q=0.5; P:120 accept iff q<1;
-    PI (DESIGN R2): exponents vanish at q = q_old = 1 → h·η; q=∞ → h·qmin."""
+    """Eq. q RMS reading: S:248 example q = 0.5 (q² = 0.25); P:120 accept
+    iff q < 1; PI (DESIGN R2) h_new = h·η·q^{−β1}·q_old^{β2}, factor clamped to
+    [1/5, 10]: exponents vanish at q = q_old = 1 → h·η; q = ∞ → h/5; q = 0 → 10h."""
     e = gold("spec_worked_values.json")["q_example"]
-    assert oracle.error_q(e["E"], e["u"], e["unew"], e["abstol"], e["reltol"]) == e["q"]
-    assert oracle.error_q([1e-3], [1.0], [1.0], 1e-3, 0.0) == 1.0
-    assert oracle.error_q([np.inf], [1.0], [1.0], 1e-3, 0.0) == np.inf
-    assert oracle.error_q([np.nan], [1.0], [1.0], 1e-3, 0.0) == np.inf
+    assert oracle.error_q2(e["E"], e["u"], e["unew"], e["abstol"], e["reltol"]) == e["q"] ** 2
+    assert oracle.error_q2([1e-3], [1.0], [1.0], 1e-3, 0.0) == 1.0
+    assert oracle.error_q2([np.inf], [1.0], [1.0], 1e-3, 0.0) == np.inf
+    assert oracle.error_q2([np.nan], [1.0], [1.0], 1e-3, 0.0) == np.inf
     for alg in ["tsit5", "rosenbrock23"]:
         C = oracle.controller(alg)
-        h, qo = oracle.pi_step(alg, True, 1.0, 1.0, 1.0)
-        assert abs(h - 0.9) < 1e-15 and qo == 1.0
-        h, _ = oracle.pi_step(alg, False, 1.0, np.inf, 1.0)
-        assert abs(h - 0.2) < 1e-15
-        h, _ = oracle.pi_step(alg, True, 1.0, 0.0, 1.0)      # growth clamp: ×10
-        assert abs(h - 10.0) < 1e-12
+        h, lo = oracle.pi_step(alg, True, 1.0, 1.0, 0.0)
+        assert abs(h - 0.9) < 1e-12 and lo == 0.0
+        h, _ = oracle.pi_step(alg, False, 1.0, np.inf, 0.0)
+        assert abs(h - 0.2) < 1e-12
+        h, lo = oracle.pi_step(alg, True, 1.0, 0.0, 0.0)      # growth clamp: ×10, q_old floored at 1e-4
+        assert abs(h - 10.0) < 1e-11 and abs(lo - L_FLOOR) < 1e-12
         # generic value: h η q^-β1 q_old^β2
         q, qold = 0.3, 0.02
-        h, qo = oracle.pi_step(alg, True, 1.0, q, qold)
-        assert abs(h - 0.9 * q ** -C["beta1"] * qold ** C["beta2"]) < 1e-14
-        assert qo == q
+        h, lo = oracle.pi_step(alg, True, 1.0, q * q, math.log2(qold))
+        assert abs(h - 0.9 * q ** -C["beta1"] * qold ** C["beta2"]) < 1e-12
+        assert abs(lo - math.log2(q)) < 1e-13
+        # reject: h / min(5, q^β1/η)
+        h, _ = oracle.pi_step(alg, False, 1.0, 1.7 ** 2, 0.0)
+        assert abs(h - 1.0 / min(5.0, 1.7 ** C["beta1"] / 0.9)) < 1e-12
         # monotone: larger q → smaller h (SPEC stepcontrol invariant)
-        hs = [oracle.pi_step(alg, True, 1.0, qq, 0.5)[0] for qq in [0.01, 0.1, 0.5, 0.9]]
+        hs = [oracle.pi_step(alg, True, 1.0, qq * qq, -1.0)[0] for qq in [0.01, 0.1, 0.5, 0.9]]
         assert all(a >= b for a, b in zip(hs, hs[1:]))
-        assert oracle.pi_step(alg, False, 1.0, 1.5, 0.5)[0] < 1.0
+        assert oracle.pi_step(alg, False, 1.0, 1.5 ** 2, -1.0)[0] < 1.0
     assert oracle.controller("tsit5")["beta1"] == 7 / 50 and oracle.controller("rosenbrock23")["beta1"] == 7 / 20
 
 
-@pytest.mark.parametrize("dtype,tol", [("f32", 2e-6), ("f64", 1e-12)])
-def test_controller_power_function(dtype, tol):
-    """DESIGN R2: the controller's x^y is a fixed polynomial 2^(y·log2 x); pinned
-    to the math library's pow over the range the controller sees, and to its
-    clamps (x ∈ [1e-30, 1e30])."""
+@pytest.mark.parametrize("dtype,tol", [("f32", 3e-7), ("f64", 1e-13)])
+def test_controller_log2_exp2(dtype, tol):
+    """DESIGN R2: the controller's log2 / exp2 are fixed polynomials over exact IEEE
+    operations; pinned to the math library over the range the controller sees."""
     rng = np.random.default_rng(1)
-    xs = np.concatenate([10.0 ** rng.uniform(-29, 29, 400), [1e-4, 0.5, 1.0, 1.5, 2.0, 0.7071, 1.4142, 1e-12]])
-    for y in [0.14, 0.08, 0.35, 0.2, -0.14, 1.0]:
-        for x in xs:
-            xt = float(np.float32(x)) if dtype == "f32" else x
-            yt = float(np.float32(y)) if dtype == "f32" else y
-            ref = xt ** yt
-            # rounding of z = y·log2(x) in T dominates for large |z|: bound ∝ (1 + |z|)
-            z = abs(yt * math.log2(xt))
-            assert abs(oracle.pw(xt, yt, dtype) - ref) <= tol * (1 + z) * ref, (x, y)
-    assert oracle.pw(1.0, 0.14, dtype) == 1.0                    # exact at x = 1
-    assert oracle.pw(0.0, 0.14, dtype) == pytest.approx(1e-30 ** 0.14, rel=1e-5)
-    assert oracle.pw(np.inf, 0.14, dtype) == pytest.approx(1e30 ** 0.14, rel=1e-5)
+    xs = np.concatenate([10.0 ** rng.uniform(-30, 30, 400), [1e-4, 0.5, 1.0, 1.5, 2.0, 0.7071, 1.4142, 1e-12]])
+    for x in xs:
+        xt = float(np.float32(x)) if dtype == "f32" else x
+        assert abs(oracle.log2_spec(xt, dtype) - math.log2(xt)) <= tol * max(1.0, abs(math.log2(xt))), x
+    for z in np.concatenate([rng.uniform(-20, 20, 400), [-3.3219, 2.3219, 0.0, 0.5, -0.5]]):
+        zt = float(np.float32(z)) if dtype == "f32" else z
+        assert abs(oracle.exp2_spec(zt, dtype) - 2.0 ** zt) <= 2 * tol * 2.0 ** zt, z
+    assert oracle.log2_spec(1.0, dtype) == 0.0 and oracle.exp2_spec(0.0, dtype) == 1.0
+    assert oracle.log2_spec(8.0, dtype) == 3.0 and oracle.exp2_spec(-3.0, dtype) == 0.125
 
 
 # ------------------------------------------------------------------------ LU --

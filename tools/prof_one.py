@@ -1,0 +1,37 @@
+#!/usr/bin/env python
+"""Run one config a few times (for ncu capture). Usage: prof_one.py NAME [N]
+NAME: c2a (Lorenz tsit5 adaptive fp32 1e-6 rho sweep), c3 (Robertson ros23 fp64
+saveat 100), c4 (stochastic Lorenz EM fp32 stats), c1 (Lorenz fp64 adaptive 1e-8)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+import paper_2304_06835_b200 as ens
+
+name = sys.argv[1]
+N = int(sys.argv[2]) if len(sys.argv) > 2 else None
+reps = 3
+if name == "c2a":
+    N = N or 10**7
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float32, N_total=N)
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6)
+elif name == "c1":
+    N = N or 1024
+    u0, p = ens.generate_inputs("lorenz", "random10", N, dtype=torch.float64, seed=0xC1)
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-8, reltol=1e-8)
+elif name == "c3":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("robertson", "random10", N, dtype=torch.float64, seed=0xC3)
+    sa = [1e5 * j / 99 for j in range(100)]
+    f = lambda: ens.solve("robertson", "rosenbrock23", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
+                          reltol=1e-8, saveat=sa)
+elif name == "c4":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("lorenz_sde_add", "const", N, dtype=torch.float32)
+    sa = [j / 10 for j in range(11)]
+    f = lambda: ens.solve("lorenz_sde_add", "em", u0, p, (0.0, 1.0), 1e-3, seed=0xC4, saveat=sa, stats=True,
+                          store_states=False)
+for _ in range(reps):
+    f()
+torch.cuda.synchronize()
+print("ok", name, N)
