@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
         L.orc_log2.restype = dbl
         L.orc_exp2.argtypes = [i32, dbl]
         L.orc_exp2.restype = dbl
+        L.orc_sincospi.argtypes = [i32, dbl, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
         L.orc_error_q2.argtypes = [i32, vp, vp, vp, dbl, dbl]
         L.orc_error_q2.restype = dbl
         L.orc_uniforms.argtypes = [i32, vp, vp]
@@ -141,6 +142,13 @@ def log2_spec(x: float, dtype="f64") -> float:
 
 def exp2_spec(z: float, dtype="f64") -> float:
     return lib().orc_exp2(DTYPES[dtype], float(z))
+
+
+def sincospi_spec(t: float, dtype="f64"):
+    """(sin πt, cos πt) by the Box–Muller polynomial (DESIGN R8)."""
+    s, c = ctypes.c_double(), ctypes.c_double()
+    lib().orc_sincospi(DTYPES[dtype], float(t), ctypes.byref(s), ctypes.byref(c))
+    return s.value, c.value
 
 
 def error_q2(E, u, unew, abstol, reltol):

@@ -183,6 +183,39 @@ static void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], ui
   for (int i = 0; i < 4; ++i) out[i] = c[i];
 }
 
+// log2 and exp2 for the step-size controller (DESIGN R2 / §4) and Box–Muller (R8):
+// L(x) = e + s·Σ_k c_k s^{2k}   (x = m·2^e, m ∈ [√½, √2), s = (m−1)/(m+1), c_k = 2/((2k+1) ln 2)),
+// 2^z  = 2^n·Σ_k (ln 2)^k f^k / k!   (n = rint(z), f = z − n).
+// Only exact IEEE operations (frexp, ldexp, rint, +, ×, ÷, fma), so they round
+// identically on every implementation (libm and CUDA pow/log2 differ in the last
+// ulp, which flips accept/reject decisions); accuracy ≈1e-7 (fp32) / 1e-13 (fp64).
+template <class T> struct PwDeg;
+template <> struct PwDeg<float> { static constexpr int L = 4, E = 7; };
+template <> struct PwDeg<double> { static constexpr int L = 8, E = 12; };
+
+template <class T> static T log2_spec(T x) {
+  const double LN2 = 0.693147180559945309417232121458176568;
+  int e;
+  T m = std::frexp(x, &e);                       // x = m·2^e, m ∈ [0.5, 1)
+  if (m < (T)0.70710678118654752440) { m = m * T(2); e -= 1; }
+  const T s = (m - T(1)) / (m + T(1));
+  const T s2 = s * s;
+  T acc = (T)(2.0 / ((2 * PwDeg<T>::L + 1) * LN2));
+  for (int k = PwDeg<T>::L - 1; k >= 0; --k) acc = std::fma(s2, acc, (T)(2.0 / ((2 * k + 1) * LN2)));
+  return std::fma(s, acc, (T)e);
+}
+template <class T> static T exp2_spec(T z) {
+  const double LN2 = 0.693147180559945309417232121458176568;
+  const T nn = std::nearbyint(z);
+  const T f = z - nn;
+  double c[16];
+  c[0] = 1.0;
+  for (int k = 1; k <= PwDeg<T>::E; ++k) c[k] = c[k - 1] * LN2 / k;   // (ln 2)^k / k!, in fp64
+  T acc = (T)c[PwDeg<T>::E];
+  for (int k = PwDeg<T>::E - 1; k >= 0; --k) acc = std::fma(f, acc, (T)c[k]);
+  return std::ldexp(acc, (int)nn);
+}
+
 // Uniforms in the open interval (0,1), exact in T (DESIGN R8).
 static float u01_f32(uint32_t w) { return ((float)(w >> 9) + 0.5f) * 1.1920928955078125e-07f; }  // 2^-23
 static double u01_f64(uint32_t wa, uint32_t wb) {
@@ -190,13 +223,41 @@ static double u01_f64(uint32_t wa, uint32_t wb) {
   return (x + 0.5) * 2.220446049250313080847263336181640625e-16;  // 2^-52
 }
 
-// cospi / sinpi of x ∈ [0,2): reduced exactly to a quarter period, then
-// evaluated with the C library's cos/sin of π·r in long double (≤1 ulp in T).
-template <class T> static void sincospi_ref(T x, T* s, T* c) {
-  const long double pi = 3.141592653589793238462643383279502884L;
-  const long double a = pi * (long double)x;
-  *s = (T)std::sin(a);
-  *c = (T)std::cos(a);
+// sin(πt), cos(πt) for t = 2U ∈ (0, 2) (DESIGN R8): exact reduction n = rint(2t),
+// r = t − n/2 ∈ [−¼, ¼]; S = r·Σ_k s_k r^{2k}, C = Σ_k c_k r^{2k} with the Taylor
+// coefficients s_k = (−1)^k π^{2k+1}/(2k+1)!, c_k = (−1)^k π^{2k}/(2k)! (fp64,
+// rounded to T once); quadrant n mod 4 selects (±S, ±C). Exact IEEE operations
+// only, so both implementations round identically.
+template <class T> struct ScDeg;
+template <> struct ScDeg<float> { static constexpr int S = 4, C = 5; };
+template <> struct ScDeg<double> { static constexpr int S = 8, C = 9; };
+template <class T> static void sincospi_spec(T t, T* sn, T* cs) {
+  const double PI = 3.141592653589793;
+  double sk[16], ck[16];
+  sk[0] = PI; ck[0] = 1.0;
+  for (int k = 1; k < 16; ++k) {
+    sk[k] = sk[k - 1] * (-(PI * PI)) / ((2.0 * k) * (2.0 * k + 1.0));
+    ck[k] = ck[k - 1] * (-(PI * PI)) / ((2.0 * k - 1.0) * (2.0 * k));
+  }
+  const T n = std::nearbyint(T(2) * t);
+  const T r = t - n * T(0.5);
+  const T r2 = r * r;
+  T ps = (T)sk[ScDeg<T>::S];
+  for (int k = ScDeg<T>::S - 1; k >= 0; --k) ps = std::fma(r2, ps, (T)sk[k]);
+  T pc = (T)ck[ScDeg<T>::C];
+  for (int k = ScDeg<T>::C - 1; k >= 0; --k) pc = std::fma(r2, pc, (T)ck[k]);
+  const T S = r * ps, C = pc;
+  switch ((int)n & 3) {
+    case 0: *sn = S; *cs = C; break;
+    case 1: *sn = C; *cs = -S; break;
+    case 2: *sn = -S; *cs = -C; break;
+    default: *sn = -C; *cs = S; break;
+  }
+}
+
+// Box–Muller radius √(−2 ln U) = √((−2 ln 2)·log2 U) with the polynomial log2 (R8).
+template <class T> static T bm_radius(T U) {
+  return std::sqrt((T)(-2.0 * 0.693147180559945309417232121458176568) * log2_spec<T>(U));
 }
 
 // Three standard normals for (trajectory gidx, step i): Box–Muller on Philox
@@ -210,11 +271,11 @@ template <> void normals3<float>(uint64_t seed, uint64_t step, uint64_t gidx, fl
   uint32_t w[4]; philox4x32_10(ctr, key, w);
   float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
   float s, c;
-  float R = std::sqrt(-2.0f * std::log(U[0]));
-  sincospi_ref<float>(2.0f * U[1], &s, &c);
+  float R = bm_radius<float>(U[0]);
+  sincospi_spec<float>(2.0f * U[1], &s, &c);
   z[0] = R * c; z[1] = R * s;
-  R = std::sqrt(-2.0f * std::log(U[2]));
-  sincospi_ref<float>(2.0f * U[3], &s, &c);
+  R = bm_radius<float>(U[2]);
+  sincospi_spec<float>(2.0f * U[3], &s, &c);
   z[2] = R * c;
 }
 template <> void normals3<double>(uint64_t seed, uint64_t step, uint64_t gidx, double z[3]) {
@@ -227,11 +288,11 @@ template <> void normals3<double>(uint64_t seed, uint64_t step, uint64_t gidx, d
     U[2 * call + 1] = u01_f64(w[2], w[3]);
   }
   double s, c;
-  double R = std::sqrt(-2.0 * std::log(U[0]));
-  sincospi_ref<double>(2.0 * U[1], &s, &c);
+  double R = bm_radius<double>(U[0]);
+  sincospi_spec<double>(2.0 * U[1], &s, &c);
   z[0] = R * c; z[1] = R * s;
-  R = std::sqrt(-2.0 * std::log(U[2]));
-  sincospi_ref<double>(2.0 * U[3], &s, &c);
+  R = bm_radius<double>(U[2]);
+  sincospi_spec<double>(2.0 * U[3], &s, &c);
   z[2] = R * c;
 }
 
@@ -328,39 +389,6 @@ static T error_q2(int n, const T* E, const T* u, const T* unew, T abstol, T relt
   T q2 = s * (T)(1.0 / n);
   if (!std::isfinite(q2)) q2 = std::numeric_limits<T>::infinity();
   return q2;
-}
-
-// log2 and exp2 for the step-size controller (DESIGN R2 / §4):
-// L(x) = e + s·Σ_k c_k s^{2k}   (x = m·2^e, m ∈ [√½, √2), s = (m−1)/(m+1), c_k = 2/((2k+1) ln 2)),
-// 2^z  = 2^n·Σ_k (ln 2)^k f^k / k!   (n = rint(z), f = z − n).
-// Only exact IEEE operations (frexp, ldexp, rint, +, ×, ÷, fma), so they round
-// identically on every implementation (libm and CUDA pow/log2 differ in the last
-// ulp, which flips accept/reject decisions); accuracy ≈1e-7 (fp32) / 1e-13 (fp64).
-template <class T> struct PwDeg;
-template <> struct PwDeg<float> { static constexpr int L = 4, E = 7; };
-template <> struct PwDeg<double> { static constexpr int L = 8, E = 12; };
-
-template <class T> static T log2_spec(T x) {
-  const double LN2 = 0.693147180559945309417232121458176568;
-  int e;
-  T m = std::frexp(x, &e);                       // x = m·2^e, m ∈ [0.5, 1)
-  if (m < (T)0.70710678118654752440) { m = m * T(2); e -= 1; }
-  const T s = (m - T(1)) / (m + T(1));
-  const T s2 = s * s;
-  T acc = (T)(2.0 / ((2 * PwDeg<T>::L + 1) * LN2));
-  for (int k = PwDeg<T>::L - 1; k >= 0; --k) acc = std::fma(s2, acc, (T)(2.0 / ((2 * k + 1) * LN2)));
-  return std::fma(s, acc, (T)e);
-}
-template <class T> static T exp2_spec(T z) {
-  const double LN2 = 0.693147180559945309417232121458176568;
-  const T nn = std::nearbyint(z);
-  const T f = z - nn;
-  double c[16];
-  c[0] = 1.0;
-  for (int k = 1; k <= PwDeg<T>::E; ++k) c[k] = c[k - 1] * LN2 / k;   // (ln 2)^k / k!, in fp64
-  T acc = (T)c[PwDeg<T>::E];
-  for (int k = PwDeg<T>::E - 1; k >= 0; --k) acc = std::fma(f, acc, (T)c[k]);
-  return std::ldexp(acc, (int)nn);
 }
 
 // Store helpers: save buffer is [k][n] for one trajectory.
@@ -778,6 +806,10 @@ double orc_log2(int dtype, double x) {
 }
 double orc_exp2(int dtype, double z) {
   return dtype == 0 ? (double)orc::exp2_spec<float>((float)z) : orc::exp2_spec<double>(z);
+}
+void orc_sincospi(int dtype, double t, double* sn, double* cs) {
+  if (dtype == 0) { float a, b; orc::sincospi_spec<float>((float)t, &a, &b); *sn = a; *cs = b; }
+  else orc::sincospi_spec<double>(t, sn, cs);
 }
 double orc_error_q2(int n, const double* E, const double* u, const double* unew, double abstol, double reltol) {
   return orc::error_q2<double>(n, E, u, unew, abstol, reltol);

@@ -164,9 +164,9 @@ def test_em_parity_and_stats(model, dtype):
     o, orc, ona, _ = oracle.solve(model, "em", u0, p, (0.0, 1.0), 1e-3, dtype=dtype, p_broadcast=True,
                                   seed=0xC4, saveat=sa)
     assert (rc == orc).all() and (na == 1000).all()
-    # normals agree to ≤ 2 ulp (libm vs CUDA log/sincospi, DESIGN R8) → a few ulp of drift
-    tol = {"f32": 1e-4, "f64": 1e-11}[dtype]
-    assert traj_relerr(g, o).max() <= tol
+    # fixed-step tolerance of the north star; the normals are specified to the bit (R8)
+    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
+    assert (g == o).mean() >= 0.99
     # fused statistics = definition applied to the GPU's own states (exact-arithmetic bound)
     mean, var, cnt = oracle.stats(g)
     np.testing.assert_allclose(st[..., 1], mean, rtol=1e-13, atol=1e-300)
@@ -201,7 +201,7 @@ def test_philox_words_bitexact():
     got = out.cpu().numpy().view(np.uint32)
     want = np.array([[int(x, 16) for x in v["out"]] for v in kat], dtype=np.uint32)
     np.testing.assert_array_equal(got, want)
-    # the EM noise stream: words bit-exact, normals within 2 ulp of the oracle's
+    # the EM noise stream: words and normals bit-exact (DESIGN R8)
     N, S = 70, 5
     for dt, npd in [(torch.float32, np.float32), (torch.float64, np.float64)]:
         words, z = ens.sde_noise(N, S, seed=0xDEADBEEF12345, dtype=dt, step0=17, index_offset=1 << 33)
@@ -215,8 +215,7 @@ def test_philox_words_bitexact():
                                         [0xDEADBEEF12345 & 0xFFFFFFFF, 0xDEADBEEF12345 >> 32])
                     np.testing.assert_array_equal(words[s, 4 * c:4 * c + 4, i], ref)
             zr = oracle.normals(0xDEADBEEF12345, g, 17, S, "f32" if dt == torch.float32 else "f64")
-            ulp = np.spacing(np.abs(zr).astype(npd))
-            assert np.all(np.abs(z[:, :, i] - zr) <= 2 * ulp)
+            np.testing.assert_array_equal(z[:, :, i], zr.astype(npd))
 
 
 # ------------------------------------------------------------------ inputs --

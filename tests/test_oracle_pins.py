@@ -392,6 +392,22 @@ def test_uniforms_exact_open_interval():
     assert d[0] == 0.5 * 2**-52 and d[1] == (2**52 - 0.5) * 2**-52 and d[1] < 1.0
 
 
+@pytest.mark.parametrize("dtype,tol", [("f32", 2.5e-7), ("f64", 1.5e-15)])   # reference sin(π·t) rounds π·t
+def test_box_muller_sincospi(dtype, tol):
+    """DESIGN R8: (sin πt, cos πt) for t ∈ (0, 2) by exact quadrant reduction and
+    Taylor polynomials on [−¼, ¼]; pinned to the math library, and exact at the
+    quadrant points."""
+    rng = np.random.default_rng(7)
+    ts = np.concatenate([rng.uniform(0, 2, 3000), np.arange(1, 16) / 8])
+    for t in ts:
+        tt = float(np.float32(t)) if dtype == "f32" else t
+        s, c = oracle.sincospi_spec(tt, dtype)
+        assert abs(s - math.sin(math.pi * tt)) <= tol and abs(c - math.cos(math.pi * tt)) <= tol, t
+    for t, (se, ce) in [(0.5, (1, 0)), (1.0, (0, -1)), (1.5, (-1, 0))]:
+        s, c = oracle.sincospi_spec(t, dtype)
+        assert abs(s - se) == 0 and abs(c - ce) == 0
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_normals_statistics(dtype):
     """Box–Muller normals (DESIGN R8): mean/variance within 4σ; KS p > 0.01."""
