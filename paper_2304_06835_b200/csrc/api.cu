@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/ens.h"
@@ -143,8 +144,16 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
         kern<<<gr, b, 0, s>>>(a);
       }
     } else {
-      if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
-      else adaptive_static_kernel<Ros23Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
+      // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); ENS_TUNE_ROS23_MINB=3
+      // caps registers for a third resident block (measured in profiles/)
+      static const int minb = [] { const char* e = getenv("ENS_TUNE_ROS23_MINB"); return e ? atoi(e) : 1; }();
+      if (minb == 3) {
+        if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T, 3><<<g, b, 0, s>>>(a);
+        else adaptive_static_kernel<Ros23Lane<M, T, false>, T, 3><<<g, b, 0, s>>>(a);
+      } else {
+        if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
+        else adaptive_static_kernel<Ros23Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
+      }
     }
   }
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;

@@ -13,8 +13,10 @@
 
 namespace ens {
 
-template <class Lane, class T>
-__global__ void __launch_bounds__(256) adaptive_static_kernel(const Args<T> a) {
+// MINB: minimum resident 256-thread blocks per SM requested from ptxas (caps
+// registers per thread; fp64 Rosenbrock23 runs at 3 instead of 2).
+template <class Lane, class T, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) adaptive_static_kernel(const Args<T> a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
   Lane L;
@@ -23,8 +25,8 @@ __global__ void __launch_bounds__(256) adaptive_static_kernel(const Args<T> a) {
   L.finish(a, i);
 }
 
-template <class Lane, class T>
-__global__ void __launch_bounds__(256) adaptive_refill_kernel(const Args<T> a) {
+template <class Lane, class T, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) adaptive_refill_kernel(const Args<T> a) {
   constexpr unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   Lane L;
