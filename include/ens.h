@@ -64,7 +64,8 @@ typedef enum {
   ENS_LORENZ_SDE_MUL = 3,  /* n=3, m=4 p=(σ,ρ,β,s), b_j = s·u_j  (DESIGN R9) */
   ENS_GBM = 4,             /* n=3, m=2 p=(r,V), dX = rX dt + VX dW */
   ENS_EXPDECAY = 5,        /* n=1, m=1 u' = −λu (closed-form test model) */
-  ENS_HARMONIC = 6         /* n=2, m=1 x' = v, v' = −ω²x (closed-form test model) */
+  ENS_HARMONIC = 6,        /* n=2, m=1 x' = v, v' = −ω²x (closed-form test model) */
+  ENS_CRN = 7              /* n=4, m=6 p=(S,D,τ,ν0,n,η), 8 Wiener: σ-factor CRN SDE, P:690-725 (DESIGN R14) */
 } ens_model;
 
 typedef enum {
@@ -80,7 +81,9 @@ typedef enum { ENS_F32 = 0, ENS_F64 = 1 } ens_dtype;
 typedef enum {
   ENS_RECIPE_RANDOM10 = 0,   /* p_j = p̄_j(1 + 0.1(2U−1)), U from SplitMix64(seed, gidx, j) */
   ENS_RECIPE_RHO_SWEEP = 1,  /* Lorenz p = (10, 21(g+1)/N_total, 8/3) */
-  ENS_RECIPE_CONST = 2       /* p = p̄ broadcast (writes m values) */
+  ENS_RECIPE_CONST = 2,      /* p = p̄ broadcast (writes m values) */
+  ENS_RECIPE_GRID = 3        /* CRN: Cartesian grid over the Table-5 ranges, L levels
+                                per parameter, L = smallest integer with L^6 >= N_total; u0 = ν0 */
 } ens_recipe;
 
 typedef struct {
@@ -169,12 +172,13 @@ ens_status ens_stats_merge(const double* gathered, int32_t R, int32_t k, int32_t
                            void* stream);
 
 /* SDE noise stream of the EM kernel (DESIGN R8), exposed for verification:
- * Philox4x32-10 words and the three Box–Muller normals that trajectory i
- * (global index per opt's index_offset / chunk fields) draws at steps
- * step0 .. step0+nsteps−1 under key `seed`. words: device uint32
- * [nsteps][4·calls][N] (calls = 1 for F32, 2 for F64) or NULL; z: device T
- * [nsteps][3][N] or NULL. Uses the same device functions as ensemble_solve. */
-ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps,
+ * Philox4x32-10 words and the nw Box–Muller normals (nw = 3 or 8) that
+ * trajectory i (global index per opt's index_offset / chunk fields) draws at
+ * steps step0 .. step0+nsteps−1 under key `seed`. words: device uint32
+ * [nsteps][4·calls][N] (calls = ceil(nw/4) for F32, ceil(nw/2) for F64) or
+ * NULL; z: device T [nsteps][nw][N] or NULL. Same device functions as
+ * ensemble_solve. ENS_E_UNSUPPORTED for other nw. */
+ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps, int32_t nw,
                          const ens_options* opt, uint32_t* words, void* z, void* stream);
 
 /* Raw Philox4x32-10 on the device: out[i] = philox(ctr[i], key[i]) for

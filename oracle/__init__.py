@@ -22,7 +22,7 @@ _SRC = _HERE / "oracle.cpp"
 _LIB = _HERE / "liboracle.so"
 
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
-          "expdecay": 5, "harmonic": 6}
+          "expdecay": 5, "harmonic": 6, "crn": 7}
 ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
@@ -66,7 +66,7 @@ def lib() -> ctypes.CDLL:
         L.orc_error_q2.argtypes = [i32, vp, vp, vp, dbl, dbl]
         L.orc_error_q2.restype = dbl
         L.orc_uniforms.argtypes = [i32, vp, vp]
-        L.orc_normals.argtypes = [i32, u64, u64, i64, i64, vp]
+        L.orc_normals.argtypes = [i32, u64, u64, i64, i64, i32, vp]
         L.orc_fixed_grid.argtypes = [dbl, dbl, dbl, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
         L.orc_lu_solve.argtypes = [i32, i32, vp, vp, vp]
         L.orc_solve.argtypes = [i32, i32, i32, i64, vp, vp, i32, vp, dbl, dbl, dbl, i32, dbl, dbl, i64, u64,
@@ -172,9 +172,9 @@ def uniforms(words, dtype="f32"):
     return out
 
 
-def normals(seed: int, gidx: int, step0: int, count: int, dtype="f64"):
-    out = np.zeros((count, 3), NP_DTYPE[dtype])
-    lib().orc_normals(DTYPES[dtype], seed, gidx, step0, count, _p(out))
+def normals(seed: int, gidx: int, step0: int, count: int, dtype="f64", nw: int = 3):
+    out = np.zeros((count, nw), NP_DTYPE[dtype])
+    lib().orc_normals(DTYPES[dtype], seed, gidx, step0, count, nw, _p(out))
     return out
 
 

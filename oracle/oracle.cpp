@@ -36,7 +36,7 @@ namespace orc {
 // ---------------------------------------------------------------- enums ----
 // Numbering mirrors include/ens.h (an interface fact, not shared code).
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
-             GBM = 4, EXPDECAY = 5, HARMONIC = 6 };
+             GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7 };
 enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
@@ -50,8 +50,32 @@ static bool dims(int model, Dims* d) {
     case GBM:            *d = {3, 2, 3, true};  return true;
     case EXPDECAY:       *d = {1, 1, 0, false}; return true;   // test model (closed form)
     case HARMONIC:       *d = {2, 1, 0, false}; return true;   // test model (closed form)
+    case CRN:            *d = {4, 6, 8, true};  return true;   // P:690-725 (σ-factor CRN, 8 Wiener)
   }
   return false;
+}
+
+template <class T> static T log2_spec(T x);
+template <class T> static T exp2_spec(T z);
+
+// Hill power x^e for the CRN model (DESIGN R14): 2^{e·L(x)} with the
+// polynomial log2 / exp2 of R2, x clamped to [1e-30, 1e30], exponent to ±120.
+template <class T> static T hill_pow(T x, T e) {
+  const T xc = std::fmin(std::fmax(x, (T)1e-30), (T)1e30);
+  const T z = std::fmin(std::fmax(e * log2_spec<T>(xc), T(-120)), T(120));
+  return exp2_spec<T>(z);
+}
+// CRN shared terms: non-negative parts (R14), Hill function, 1/τ.
+template <class T> struct CrnTerms { T sp, a3p, hill, itau; };
+template <class T> static CrnTerms<T> crn_terms(const T* y, const T* p) {
+  CrnTerms<T> c;
+  c.sp = std::fmax(y[0], T(0));
+  c.a3p = std::fmax(y[3], T(0));
+  const T a = hill_pow<T>(p[0] * c.sp, p[4]);
+  const T b = hill_pow<T>(p[1] * c.a3p, p[4]);
+  c.hill = a / ((a + b) + T(1));
+  c.itau = T(1) / p[2];
+  return c;
 }
 
 // --------------------------------------------------------------- models ----
@@ -86,6 +110,15 @@ static void rhs(int model, const T* y, const T* p, T /*t*/, T* f) {
     }
     case EXPDECAY: f[0] = (-p[0]) * y[0]; return;          // u' = −λu
     case HARMONIC: f[0] = y[1]; f[1] = -(p[0] * y[0]); return;  // x' = v, v' = −ω² x
+    case CRN: {
+      // P:692-705 drift, p = (S, D, τ, ν0, n, η), y = ([σ], [A1], [A2], [A3])
+      const CrnTerms<T> c = crn_terms<T>(y, p);
+      f[0] = (p[3] + c.hill) - y[0];
+      f[1] = (y[0] - y[1]) * c.itau;
+      f[2] = (y[1] - y[2]) * c.itau;
+      f[3] = (y[2] - y[3]) * c.itau;
+      return;
+    }
   }
 }
 
@@ -97,6 +130,31 @@ static void diffusion(int model, const T* y, const T* p, T /*t*/, T* b) {
     case LORENZ_SDE_MUL: for (int j = 0; j < 3; ++j) b[j] = p[3] * y[j]; return;   // R9: b_j = s u_j
     case GBM:            for (int j = 0; j < 3; ++j) b[j] = p[1] * y[j]; return;   // V X
   }
+}
+
+// Noise increment x += G(y) ΔW in the model's canonical order:
+// diagonal models x_j = fma(b_j, ΔW_j, x_j); CRN row i carries
+// columns 2i, 2i+1: x_i = fma(G_i,2i, ΔW_2i, x_i); x_i = fma(G_i,2i+1, ΔW_2i+1, x_i).
+template <class T>
+static void noise_update(int model, const T* y, const T* p, T t, const T* dW, T* x) {
+  if (model == CRN) {
+    const CrnTerms<T> c = crn_terms<T>(y, p);
+    const T eta = p[5];
+    T G[8];
+    G[0] = eta * std::sqrt(std::fmax(p[3] + c.hill, T(0)));
+    G[1] = -(eta * std::sqrt(c.sp));
+    const T r1 = eta * std::sqrt(c.sp * c.itau), r2 = eta * std::sqrt(std::fmax(y[1], T(0)) * c.itau);
+    const T r3 = eta * std::sqrt(std::fmax(y[2], T(0)) * c.itau), r4 = eta * std::sqrt(c.a3p * c.itau);
+    G[2] = r1; G[3] = -r2; G[4] = r2; G[5] = -r3; G[6] = r3; G[7] = -r4;
+    for (int i = 0; i < 4; ++i) {
+      x[i] = std::fma(G[2 * i], dW[2 * i], x[i]);
+      x[i] = std::fma(G[2 * i + 1], dW[2 * i + 1], x[i]);
+    }
+    return;
+  }
+  T b[8];
+  diffusion<T>(model, y, p, t, b);
+  for (int j = 0; j < 3; ++j) x[j] = std::fma(b[j], dW[j], x[j]);
 }
 
 // Analytic Jacobian ∂f/∂u (row-major J[i*n+j] = ∂f_i/∂u_j). The paper uses
@@ -260,40 +318,41 @@ template <class T> static T bm_radius(T U) {
   return std::sqrt((T)(-2.0 * 0.693147180559945309417232121458176568) * log2_spec<T>(U));
 }
 
-// Three standard normals for (trajectory gidx, step i): Box–Muller on Philox
-// uniforms; counter = (step, gidx lo, gidx hi, call), key = (seed lo, seed hi)
-// (DESIGN R8). fp32: one call, pairs (U0,U1),(U2,U3); fp64: two calls, each
-// pair (U_a,U_b) from one call. Fourth normal dropped.
-template <class T> static void normals3(uint64_t seed, uint64_t step, uint64_t gidx, T z[3]);
-template <> void normals3<float>(uint64_t seed, uint64_t step, uint64_t gidx, float z[3]) {
+// nw standard normals for (trajectory gidx, step): Box–Muller pairs in order
+// from Philox calls c = 0, 1, … with counter = (step, gidx lo, gidx hi, c) and
+// key = (seed lo, seed hi) (DESIGN R8). fp32: each call gives two pairs
+// (U0,U1), (U2,U3); fp64: each call gives one pair (U_a from words 0,1; U_b
+// from words 2,3). Each pair gives (R·cos, R·sin); surplus normals are dropped.
+template <class T> static void normalsN(uint64_t seed, uint64_t step, uint64_t gidx, int nw, T* z);
+template <> void normalsN<float>(uint64_t seed, uint64_t step, uint64_t gidx, int nw, float* z) {
   const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), 0u};
-  uint32_t w[4]; philox4x32_10(ctr, key, w);
-  float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
-  float s, c;
-  float R = bm_radius<float>(U[0]);
-  sincospi_spec<float>(2.0f * U[1], &s, &c);
-  z[0] = R * c; z[1] = R * s;
-  R = bm_radius<float>(U[2]);
-  sincospi_spec<float>(2.0f * U[3], &s, &c);
-  z[2] = R * c;
-}
-template <> void normals3<double>(uint64_t seed, uint64_t step, uint64_t gidx, double z[3]) {
-  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  double U[4];
-  for (uint32_t call = 0; call < 2; ++call) {
-    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), call};
+  for (int c = 0; 4 * c < nw; ++c) {
+    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)c};
     uint32_t w[4]; philox4x32_10(ctr, key, w);
-    U[2 * call] = u01_f64(w[0], w[1]);
-    U[2 * call + 1] = u01_f64(w[2], w[3]);
+    float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
+    for (int q = 0; q < 2; ++q) {
+      const int id = 4 * c + 2 * q;
+      if (id >= nw) break;
+      float sn, cs;
+      const float R = bm_radius<float>(U[2 * q]);
+      sincospi_spec<float>(2.0f * U[2 * q + 1], &sn, &cs);
+      z[id] = R * cs;
+      if (id + 1 < nw) z[id + 1] = R * sn;
+    }
   }
-  double s, c;
-  double R = bm_radius<double>(U[0]);
-  sincospi_spec<double>(2.0 * U[1], &s, &c);
-  z[0] = R * c; z[1] = R * s;
-  R = bm_radius<double>(U[2]);
-  sincospi_spec<double>(2.0 * U[3], &s, &c);
-  z[2] = R * c;
+}
+template <> void normalsN<double>(uint64_t seed, uint64_t step, uint64_t gidx, int nw, double* z) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (int c = 0; 2 * c < nw; ++c) {
+    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)c};
+    uint32_t w[4]; philox4x32_10(ctr, key, w);
+    const double Ua = u01_f64(w[0], w[1]), Ub = u01_f64(w[2], w[3]);
+    double sn, cs;
+    const double R = bm_radius<double>(Ua);
+    sincospi_spec<double>(2.0 * Ub, &sn, &cs);
+    z[2 * c] = R * cs;
+    if (2 * c + 1 < nw) z[2 * c + 1] = R * sn;
+  }
 }
 
 // ------------------------------------------------------ fixed-step grid ----
@@ -683,7 +742,10 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
 template <class T>
 static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const int n = tr.n, model = o.model;
-  T u[8], a[8], b[8], z[3];
+  Dims d;
+  dims(model, &d);
+  const int nw = d.nw;
+  T u[8], a[8], x[8], z[8], dW[8];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
   int64_t nsteps; double h_last;
@@ -699,12 +761,11 @@ static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
     const T h = last ? hl : hdt, sh = last ? sq_l : sq_dt;
     const T t = (T)(o.t0 + (double)i * o.dt);
     rhs<T>(model, u, p, t, a);
-    diffusion<T>(model, u, p, t, b);
-    normals3<T>(o.seed, (uint64_t)i, tr.gidx, z);
-    for (int j = 0; j < n; ++j) {
-      const T dW = sh * z[j];
-      u[j] = std::fma(b[j], dW, std::fma(h, a[j], u[j]));
-    }
+    normalsN<T>(o.seed, (uint64_t)i, tr.gidx, nw, z);
+    for (int q = 0; q < nw; ++q) dW[q] = sh * z[q];              // ΔW = √h Z
+    for (int j = 0; j < n; ++j) x[j] = std::fma(h, a[j], u[j]);   // u + h a
+    noise_update<T>(model, u, p, t, dW, x);                       // + G ΔW
+    for (int j = 0; j < n; ++j) u[j] = x[j];
     tr.n_accept++;
     while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
   }
@@ -823,10 +884,10 @@ void orc_uniforms(int dtype, const uint32_t* w4, void* out) {
   else { ((double*)out)[0] = orc::u01_f64(w4[0], w4[1]); ((double*)out)[1] = orc::u01_f64(w4[2], w4[3]); }
 }
 // Normals for `count` consecutive steps of trajectory gidx: out[count][3].
-void orc_normals(int dtype, uint64_t seed, uint64_t gidx, int64_t step0, int64_t count, void* out) {
+void orc_normals(int dtype, uint64_t seed, uint64_t gidx, int64_t step0, int64_t count, int nw, void* out) {
   for (int64_t s = 0; s < count; ++s) {
-    if (dtype == 0) orc::normals3<float>(seed, (uint64_t)(step0 + s), gidx, (float*)out + 3 * s);
-    else orc::normals3<double>(seed, (uint64_t)(step0 + s), gidx, (double*)out + 3 * s);
+    if (dtype == 0) orc::normalsN<float>(seed, (uint64_t)(step0 + s), gidx, nw, (float*)out + nw * s);
+    else orc::normalsN<double>(seed, (uint64_t)(step0 + s), gidx, nw, (double*)out + nw * s);
   }
 }
 

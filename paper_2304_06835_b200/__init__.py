@@ -21,10 +21,10 @@ _PKG = Path(__file__).resolve().parent
 _LIB_PATH = _PKG / "libens.so"
 
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4, "expdecay": 5,
-          "harmonic": 6}
+          "harmonic": 6, "crn": 7}
 ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2}
 DTYPES = {torch.float32: 0, torch.float64: 1}
-RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2}
+RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
 RETCODES = {0: "Success", 1: "MaxIters", 2: "DtLessThanMin", 3: "Diverged", 4: "Singular"}
 
 
@@ -81,7 +81,7 @@ def lib() -> ctypes.CDLL:
         L.ens_stats_finalize.restype = i32
         L.ens_stats_merge.argtypes = [vp, i32, i32, i32, vp, vp]
         L.ens_stats_merge.restype = i32
-        L.ens_sde_noise.argtypes = [i32, u64, i64, i64, i64, ctypes.POINTER(_Options), vp, vp, vp]
+        L.ens_sde_noise.argtypes = [i32, u64, i64, i64, i64, i32, ctypes.POINTER(_Options), vp, vp, vp]
         L.ens_sde_noise.restype = i32
         L.ens_philox4x32_10.argtypes = [vp, vp, vp, i64, vp]
         L.ens_philox4x32_10.restype = i32
@@ -295,16 +295,16 @@ def stats_merge(gathered: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 def sde_noise(N: int, nsteps: int, *, seed: int, dtype=torch.float32, step0: int = 0, index_offset: int = 0,
-              chunk_len: int = 0, chunk_stride: int = 0, device=None, stream=None):
-    """ens_sde_noise: (Philox words [nsteps, 4·calls, N] uint32-as-int32, normals [nsteps, 3, N])."""
+              chunk_len: int = 0, chunk_stride: int = 0, nw: int = 3, device=None, stream=None):
+    """ens_sde_noise: (Philox words [nsteps, 4·calls, N] uint32-as-int32, normals [nsteps, nw, N])."""
     dev = torch.device(device or "cuda")
-    calls = 1 if dtype == torch.float32 else 2
+    calls = (nw + 3) // 4 if dtype == torch.float32 else (nw + 1) // 2
     words = torch.empty((nsteps, 4 * calls, N), dtype=torch.int32, device=dev)
-    z = torch.empty((nsteps, 3, N), dtype=dtype, device=dev)
+    z = torch.empty((nsteps, nw, N), dtype=dtype, device=dev)
     opt = _options(0, 0, 0, 0, 0, None, 0, 0, 0, index_offset, chunk_len, chunk_stride)
     with torch.cuda.device(dev):
-        st = lib().ens_sde_noise(DTYPES[dtype], int(seed), int(N), int(step0), int(nsteps), ctypes.byref(opt),
-                                 _ptr(words), _ptr(z), _stream_ptr(stream))
+        st = lib().ens_sde_noise(DTYPES[dtype], int(seed), int(N), int(step0), int(nsteps), int(nw),
+                                 ctypes.byref(opt), _ptr(words), _ptr(z), _stream_ptr(stream))
     if st:
         raise EnsError(st, "ens_sde_noise")
     return words, z

@@ -33,6 +33,7 @@ bool model_dims(int model, int* n, int* m, int* nw) {
     case ENS_GBM: *n = 3; *m = 2; *nw = 3; return true;
     case ENS_EXPDECAY: *n = 1; *m = 1; *nw = 0; return true;
     case ENS_HARMONIC: *n = 2; *m = 1; *nw = 0; return true;
+    case ENS_CRN: *n = 4; *m = 6; *nw = 8; return true;
   }
   return false;
 }
@@ -123,6 +124,9 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
         kern<<<gr, b, 0, s>>>(a);
       }
     } else {
+      // (a two-trajectories-per-thread f2 variant of the adaptive step measured 4 % slower:
+      //  90 vs 48 registers halves residency, per-lane control flow stays scalar —
+      //  profiles/pair_adaptive_r01.log; the fixed-step kernel is where packing pays)
       if (save) adaptive_static_kernel<Tsit5Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
       else adaptive_static_kernel<Tsit5Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
     }
@@ -144,9 +148,12 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
         kern<<<gr, b, 0, s>>>(a);
       }
     } else {
-      // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); ENS_TUNE_ROS23_MINB=3
-      // caps registers for a third resident block (measured in profiles/)
-      static const int minb = [] { const char* e = getenv("ENS_TUNE_ROS23_MINB"); return e ? atoi(e) : 1; }();
+      // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
+      // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log). ENS_TUNE_ROS23_MINB=1 reverts.
+      static const int minb = [] {
+        const char* e = getenv("ENS_TUNE_ROS23_MINB");
+        return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
+      }();
       if (minb == 3) {
         if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T, 3><<<g, b, 0, s>>>(a);
         else adaptive_static_kernel<Ros23Lane<M, T, false>, T, 3><<<g, b, 0, s>>>(a);
@@ -177,6 +184,7 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_LORENZ_SDE_ADD: return run_sde<LorenzSDE<false>, T>(a, opt, s);
     case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(a, opt, s);
     case ENS_GBM: return run_sde<GBM, T>(a, opt, s);
+    case ENS_CRN: return run_sde<CRN, T>(a, opt, s);
   }
   return ENS_E_INVALID_ARG;
 }
@@ -403,14 +411,30 @@ ens_status ens_generate_inputs(ens_model model, ens_dtype dtype, ens_recipe reci
   InputSpec sp{};
   int nw;
   if (!model_dims(model, &sp.n, &sp.m, &nw) || N < 1 || !u0 || !p) return ENS_E_INVALID_ARG;
-  if (recipe < ENS_RECIPE_RANDOM10 || recipe > ENS_RECIPE_CONST) return ENS_E_INVALID_ARG;
+  if (recipe < ENS_RECIPE_RANDOM10 || recipe > ENS_RECIPE_GRID) return ENS_E_INVALID_ARG;
   if (recipe == ENS_RECIPE_RHO_SWEEP && model != ENS_LORENZ) return ENS_E_UNSUPPORTED;
+  if ((recipe == ENS_RECIPE_GRID) != (model == ENS_CRN)) return ENS_E_UNSUPPORTED;
   // p̄ and ū0 of DESIGN §6 (same table as synth/inputs.py)
+  // p̄ and ū0 of DESIGN §6 (same table as synth/inputs.py); CRN: Table-5 ranges (lo, hi)
   static const double PB[7][4] = {{10.0, 28.0, 8.0 / 3.0, 0}, {0.04, 3e7, 1e4, 0}, {10.0, 28.0, 8.0 / 3.0, 0.1},
                                   {10.0, 28.0, 8.0 / 3.0, 0.1}, {1.5, 0.01, 0, 0}, {1.0, 0, 0, 0}, {1.0, 0, 0, 0}};
   static const double UB[7][3] = {{1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {0.1, 0.1, 0.1}, {1, 0, 0}, {1, 0, 0}};
-  for (int j = 0; j < 4; ++j) sp.pbar[j] = PB[model][j];
-  for (int j = 0; j < 3; ++j) sp.ubar[j] = UB[model][j];
+  static const double CRN_LO[6] = {0.1, 0.1, 0.1, 0.01, 2.0, 0.001}, CRN_HI[6] = {100.0, 100.0, 100.0, 0.2, 4.0, 0.1};
+  if (model == ENS_CRN) {
+    for (int j = 0; j < 6; ++j) { sp.lo[j] = CRN_LO[j]; sp.hi[j] = CRN_HI[j]; }
+    const int64_t nt = N_total > 0 ? N_total : N;
+    int64_t L = 2;
+    while (true) {                       // smallest L >= 2 with L^6 >= N_total
+      int64_t pw = 1;
+      for (int j = 0; j < 6; ++j) pw *= L;
+      if (pw >= nt) break;
+      ++L;
+    }
+    sp.levels = L;
+  } else {
+    for (int j = 0; j < 4; ++j) sp.pbar[j] = PB[model][j];
+    for (int j = 0; j < 3; ++j) sp.ubar[j] = UB[model][j];
+  }
   sp.recipe = recipe;
   sp.n_total = (double)(N_total > 0 ? N_total : N);
   const int64_t off = opt ? opt->index_offset : 0, cl = opt ? opt->chunk_len : 0, cs = opt ? opt->chunk_stride : 0;
@@ -454,14 +478,20 @@ ens_status ens_stats_merge(const double* gathered, int32_t R, int32_t k, int32_t
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 
-ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps,
+ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps, int32_t nw,
                          const ens_options* opt, uint32_t* words, void* z, void* stream) {
   if (N < 1 || nsteps < 0 || step0 < 0 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (nw != 3 && nw != 8) return ENS_E_UNSUPPORTED;
   const int64_t off = opt ? opt->index_offset : 0, cl = opt ? opt->chunk_len : 0, cs = opt ? opt->chunk_stride : 0;
   const dim3 g((unsigned)cdiv(N, kBlock));
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == ENS_F32) sde_noise_kernel<float><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
-  else sde_noise_kernel<double><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
+  if (dtype == ENS_F32) {
+    if (nw == 3) sde_noise_kernel<float, 3><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
+    else sde_noise_kernel<float, 8><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
+  } else {
+    if (nw == 3) sde_noise_kernel<double, 3><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
+    else sde_noise_kernel<double, 8><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 

@@ -22,6 +22,8 @@ struct InputSpec {
   int n, m, recipe;
   double pbar[8], ubar[8];
   double n_total;
+  double lo[8], hi[8];   // grid recipe ranges
+  int64_t levels;        // grid recipe levels per parameter
 };
 
 template <class T>
@@ -40,6 +42,17 @@ __global__ void generate_inputs_kernel(InputSpec s, uint64_t seed, int64_t N, in
     p[i] = (T)10.0;
     p[(size_t)N + i] = (T)((21.0 * (double)(g + 1)) / s.n_total);
     p[(size_t)2 * N + i] = (T)(8.0 / 3.0);
+  } else if (s.recipe == 3) {   // grid (CRN): digit j of g in base L, parameter j fastest-first
+    int64_t r = g;
+    double nu0 = 0.0;
+    for (int j = 0; j < s.m; ++j) {
+      const int64_t d = r % s.levels;
+      r /= s.levels;
+      const double v = (s.hi[j] - s.lo[j]) * ((double)d / (double)(s.levels - 1)) + s.lo[j];
+      p[(size_t)j * N + i] = (T)v;
+      if (j == 3) nu0 = v;
+    }
+    for (int c = 0; c < s.n; ++c) u0[(size_t)c * N + i] = (T)nu0;   // u0 = ν0
   } else if (i == 0) {          // const: p̄ broadcast
     for (int j = 0; j < s.m; ++j) p[j] = (T)s.pbar[j];
   }

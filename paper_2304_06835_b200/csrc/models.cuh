@@ -66,6 +66,74 @@ struct GBM {  // dX = rX dt + VX dW (diagonal, 3 independent componen
   }
 };
 
+// Noise increment x += G(y) ΔW in the model's canonical order.
+// Diagonal models: x_j = fma(b_j, ΔW_j, x_j).
+template <class M, class T>
+__device__ __forceinline__ void diag_noise(const T (&y)[M::n], const T (&p)[M::m], T t, const T (&dW)[M::nw],
+                                           T (&x)[M::n]) {
+  T b[M::n];
+  M::g(y, p, t, b);
+#pragma unroll
+  for (int j = 0; j < M::n; ++j) x[j] = fmaT(b[j], dW[j], x[j]);
+}
+
+// σ-factor stress-response CRN as a chemical Langevin SDE:
+// y = ([σ], [A1], [A2], [A3]), p = (S, D, τ, ν0, n, η), 8 Wiener processes.
+//   d[σ]  = (ν0 + H − [σ]) dt + η√(ν0 + H) dW1 − η√[σ] dW2,  H = (S[σ])^n / ((S[σ])^n + (D[A3])^n + 1)
+//   d[A_k] = ([A_{k−1}] − [A_k])/τ dt + η√([A_{k−1}]/τ) dW_{2k+1} − η√([A_k]/τ) dW_{2k+2}
+// DESIGN R14: non-negative parts inside powers and square roots; x^n by the
+// polynomial 2^{n·L(x)} of R2 (x ∈ [1e-30, 1e30], exponent clamped to ±120).
+struct CRN {
+  static constexpr int n = 4, m = 6, nw = 8;
+  template <class T> __device__ __forceinline__ static T hill_pow(T x, T e) {
+    const T xc = minT(maxT(x, T(1e-30)), T(1e30));
+    const T z = minT(maxT(e * log2_spec<T>(xc), T(-120)), T(120));
+    return exp2_spec<T>(z);
+  }
+  template <class T> __device__ __forceinline__ static void terms(const T (&y)[4], const T (&p)[m], T& sp, T& a3p,
+                                                                  T& hill, T& itau) {
+    sp = maxT(y[0], T(0));
+    a3p = maxT(y[3], T(0));
+    const T a = hill_pow<T>(p[0] * sp, p[4]);
+    const T b = hill_pow<T>(p[1] * a3p, p[4]);
+    hill = a / ((a + b) + T(1));
+    itau = T(1) / p[2];
+  }
+  template <class T> __device__ __forceinline__ static void f(const T (&y)[4], const T (&p)[m], T, T (&o)[4]) {
+    T sp, a3p, hill, itau;
+    terms<T>(y, p, sp, a3p, hill, itau);
+    o[0] = (p[3] + hill) - y[0];
+    o[1] = (y[0] - y[1]) * itau;
+    o[2] = (y[1] - y[2]) * itau;
+    o[3] = (y[2] - y[3]) * itau;
+  }
+  // row i carries columns 2i, 2i+1: x_i = fma(G_i,2i, ΔW_2i, x_i); x_i = fma(G_i,2i+1, ΔW_2i+1, x_i)
+  template <class T> __device__ __forceinline__ static void noise(const T (&y)[4], const T (&p)[m], T,
+                                                                  const T (&dW)[8], T (&x)[4]) {
+    T sp, a3p, hill, itau;
+    terms<T>(y, p, sp, a3p, hill, itau);
+    const T eta = p[5];
+    T G[8];
+    G[0] = eta * sqrtT(maxT(p[3] + hill, T(0)));
+    G[1] = -(eta * sqrtT(sp));
+    const T r1 = eta * sqrtT(sp * itau), r2 = eta * sqrtT(maxT(y[1], T(0)) * itau);
+    const T r3 = eta * sqrtT(maxT(y[2], T(0)) * itau), r4 = eta * sqrtT(a3p * itau);
+    G[2] = r1; G[3] = -r2; G[4] = r2; G[5] = -r3; G[6] = r3; G[7] = -r4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] = fmaT(G[2 * i], dW[2 * i], x[i]);
+      x[i] = fmaT(G[2 * i + 1], dW[2 * i + 1], x[i]);
+    }
+  }
+};
+
+template <class M, class T>
+__device__ __forceinline__ void apply_noise(const T (&y)[M::n], const T (&p)[M::m], T t, const T (&dW)[M::nw],
+                                            T (&x)[M::n]) {
+  if constexpr (M::nw == 8) M::noise(y, p, t, dW, x);
+  else diag_noise<M, T>(y, p, t, dW, x);
+}
+
 struct ExpDecay {  // u' = −λu
   static constexpr int n = 1, m = 1, nw = 0;
   template <class T> __device__ __forceinline__ static void f(const T (&y)[1], const T (&p)[1], T, T (&o)[1]) {

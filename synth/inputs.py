@@ -33,8 +33,19 @@ MODELS = {
     "gbm":            dict(pbar=(1.5, 0.01), u0=(0.1, 0.1, 0.1)),
     "expdecay":       dict(pbar=(1.0,), u0=(1.0,)),
     "harmonic":       dict(pbar=(1.0,), u0=(1.0, 0.0)),
+    # σ-factor CRN: p = (S, D, τ, ν0, n, η); Table 5 ranges; u0 = ν0
+    "crn":            dict(pbar=(1.0, 1.0, 1.0, 0.1, 3.0, 0.05), u0=(0.1, 0.1, 0.1, 0.1),
+                           lo=(0.1, 0.1, 0.1, 0.01, 2.0, 0.001), hi=(100.0, 100.0, 100.0, 0.2, 4.0, 0.1)),
 }
-RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2}
+RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
+
+
+def grid_levels(n_total: int, m: int = 6) -> int:
+    """Smallest L >= 2 with L^m >= n_total (levels per parameter of the grid recipe)."""
+    L = 2
+    while L**m < n_total:
+        L += 1
+    return L
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
 
@@ -84,6 +95,20 @@ def make_inputs(model: str, recipe: str, N: int, *, seed: int = 0, dtype: str = 
         for j in range(m):
             U = uniform(seed, g, j)
             p[j] = pbar[j] * (1.0 + 0.1 * (2.0 * U - 1.0))
+    elif recipe == "grid":
+        # Cartesian product of uniformly spaced levels ("each of the parameters is uniformly
+        # sampled and the set of the Cartesian products … is simulated"); parameter 0 varies fastest
+        if model != "crn":
+            raise ValueError("grid is the CRN recipe")
+        L = grid_levels(N if N_total is None else N_total, m)
+        lo, hi = spec["lo"], spec["hi"]
+        r = g.astype(np.int64).copy()
+        for j in range(m):
+            d = r % L
+            r //= L
+            p[j] = (hi[j] - lo[j]) * (d.astype(np.float64) / float(L - 1)) + lo[j]
+        for c in range(n):
+            u0[c, :] = p[3].astype(T)                      # u0 = ν0
     elif recipe == "rho_sweep":
         if model != "lorenz":
             raise ValueError("rho_sweep is a Lorenz recipe")

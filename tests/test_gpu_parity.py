@@ -255,6 +255,22 @@ def test_retcodes_and_isolation():
     assert (rc[[0, 1, 2, 3, 4]] == 1).all() and ((na + nr) == 20).all()
 
 
+@pytest.mark.parametrize("N", [1, 2, 3, 513, 1025])
+def test_paired_fp32_kernels_ragged(N):
+    """fp32 fixed and adaptive kernels carry two trajectories per thread: odd N
+    leaves a dead partner lane; results must equal the oracle and the scalar
+    (refill) path bit for bit."""
+    u0, p = make_inputs("lorenz", "random10", N, seed=N + 7, dtype="f32")
+    u0[0, N // 2] = np.nan                         # a diverged lane next to a live partner
+    g, rc, na, nr, _ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3)
+    o, orc, ona, onr = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f32")
+    np.testing.assert_array_equal(rc, orc)
+    np.testing.assert_array_equal(na, ona)
+    ok = rc == 0
+    assert traj_relerr(g[..., ok], o[..., ok]).max() <= TOL_FIXED["f32"]
+    np.testing.assert_array_equal(g[..., ~ok], o[..., ~ok])     # diverged lane keeps u0
+
+
 @pytest.mark.parametrize("N", [1, 31, 32, 33, 255, 257])
 def test_small_and_ragged_sizes(N):
     u0, p = make_inputs("lorenz", "random10", N, seed=N, dtype="f64")
@@ -319,3 +335,41 @@ def test_solve_host_matches_device():
                                 reltol=1e-6, refill=True)
     g, rc, *_ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6)
     np.testing.assert_array_equal(uh.numpy(), g[0])
+
+
+# ------------------------------------------------------------ CRN (NEXT-3) --
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_crn_em_parity_and_stats(dtype):
+    """σ-factor CRN SDE: 4 states, 8 Wiener processes (non-diagonal
+    noise), grid parameters over Table 5 (10^6-point grid, a 1500-trajectory
+    window of it), dt = 0.1 as in P:725 over [0, 100], saveat every 10."""
+    N, off = 1500, 123456
+    u0, p = make_inputs("crn", "grid", N, dtype=dtype, N_total=10**6, index_offset=off)
+    sa = np.linspace(0.0, 100.0, 11)
+    g, rc, na, _, st = gpu("crn", "em", u0, p, (0.0, 100.0), 0.1, seed=0x5EED, saveat=sa, stats=True,
+                           index_offset=off)
+    o, orc, ona, _ = oracle.solve("crn", "em", u0, p, (0.0, 100.0), 0.1, dtype=dtype, seed=0x5EED, saveat=sa,
+                                  gidx=np.arange(off, off + N))
+    np.testing.assert_array_equal(rc, orc)
+    assert (na == 1000).all()
+    ok = rc == 0
+    assert ok.mean() > 0.99
+    assert traj_relerr(g[..., ok], o[..., ok]).max() <= TOL_FIXED[dtype]
+    mean, var, _ = oracle.stats(g)
+    np.testing.assert_allclose(st[..., 1], mean, rtol=1e-12, atol=1e-300)
+
+
+def test_crn_inputs_and_noise_bitwise():
+    import torch
+
+    import paper_2304_06835_b200 as ens
+    for dt, name in [(torch.float32, "f32"), (torch.float64, "f64")]:
+        u0g, pg = ens.generate_inputs("crn", "grid", 3000, dtype=dt, N_total=10**6, index_offset=777)
+        u0h, ph = make_inputs("crn", "grid", 3000, dtype=name, N_total=10**6, index_offset=777)
+        np.testing.assert_array_equal(u0g.cpu().numpy(), u0h)
+        np.testing.assert_array_equal(pg.cpu().numpy(), ph)
+        w, z = ens.sde_noise(40, 3, seed=99, dtype=dt, step0=5, index_offset=1000, nw=8)
+        z = z.cpu().numpy()
+        for i in [0, 17, 39]:
+            zr = oracle.normals(99, 1000 + i, 5, 3, name, nw=8)
+            np.testing.assert_array_equal(z[:, :, i], zr)

@@ -510,3 +510,66 @@ def test_retcodes():
     out, rc, na, nr = oracle.solve("lorenz", "tsit5", u0[:, :1], p[:, :1], (0, 1), 1e-3, adaptive=True,
                                    abstol=1e-8, reltol=1e-8, max_steps=10)
     assert rc[0] == 1 and na[0] + nr[0] == 10
+
+
+# ------------------------------------------------------------ CRN (NEXT-3) --
+CRN_P = [2.0, 3.0, 5.0, 0.1, 2.0, 0.05]      # (S, D, τ, ν0, n, η)
+
+
+def test_crn_drift_worked_values():
+    """P:692-705 drift by direct substitution: Hill term (Sσ)^n / ((Sσ)^n + (D A3)^n + 1)."""
+    S, D, tau, nu0, n, eta = CRN_P
+    y = np.array([0.5, 0.2, 0.3, 1.0 / 3.0])       # Sσ = 1, D·A3 = 1 → H = 1/3
+    f = oracle.rhs("crn", y, CRN_P)
+    np.testing.assert_allclose(f, [nu0 + 1 / 3 - 0.5, (0.5 - 0.2) / tau, (0.2 - 0.3) / tau, (0.3 - 1 / 3) / tau],
+                               rtol=1e-12)
+    f0 = oracle.rhs("crn", np.zeros(4), CRN_P)      # σ = 0 → H = 0 (R14 clamps)
+    np.testing.assert_allclose(f0, [nu0, 0, 0, 0], atol=1e-50)
+    y2 = np.array([1.5, 0.0, 0.0, 0.0])              # Sσ = 3, A3 = 0 → H = 9/10
+    assert abs(oracle.rhs("crn", y2, CRN_P)[0] - (nu0 + 0.9 - 1.5)) < 1e-12
+    # non-integer Hill exponent
+    p = list(CRN_P); p[4] = 2.5
+    y3 = np.array([0.8, 0.1, 0.1, 0.4])
+    a, b = (2.0 * 0.8) ** 2.5, (3.0 * 0.4) ** 2.5
+    assert abs(oracle.rhs("crn", y3, p)[0] - (0.1 + a / (a + b + 1) - 0.8)) < 1e-12
+
+
+def test_crn_deterministic_steady_state():
+    """η = 0: EM is explicit Euler on the drift; it relaxes to the fixed point
+    A1 = A2 = A3 = σ*, σ* = ν0 + (Sσ*)^n / ((Sσ*)^n + (Dσ*)^n + 1), found here by bisection."""
+    S, D, tau, nu0, n, eta = CRN_P
+    g = lambda s: nu0 + (S * s) ** n / ((S * s) ** n + (D * s) ** n + 1) - s
+    lo, hi = 1e-9, 2.0
+    assert g(lo) > 0 > g(hi)
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if g(mid) > 0 else (lo, mid)
+    p = list(CRN_P); p[5] = 0.0; p[2] = 0.5      # τ = 0.5: stable fixed point (slow τ oscillates)
+    out, rc, na, _ = oracle.solve("crn", "em", np.full((4, 1), nu0), np.array(p)[:, None], (0, 300), 0.1)
+    assert rc[0] == 0 and na[0] == 3000
+    np.testing.assert_allclose(out[0, :, 0], [lo] * 4, rtol=1e-9)
+    # and the same trajectory by fixed-step Tsit5 at t = 20 agrees to O(dt) (Euler is order 1)
+    eu, *_ = oracle.solve("crn", "em", np.full((4, 1), nu0), np.array(p)[:, None], (0, 20), 1e-3)
+    ts, *_ = oracle.solve("crn", "tsit5", np.full((4, 1), nu0), np.array(p)[:, None], (0, 20), 1e-2)
+    assert np.abs(eu - ts).max() < 5e-3 * np.abs(ts).max()
+
+
+def test_crn_one_step_noise_variance():
+    """One EM step from a fixed state over many independent paths: the increment
+    variance is h·η²·(ν0 + H + σ) for [σ] and h·η²·(A_{k−1} + A_k)/τ for [A_k]
+    (the two Wiener terms of each equation)."""
+    S, D, tau, nu0, n, eta = CRN_P
+    y = np.array([0.5, 0.2, 0.3, 1.0 / 3.0])
+    N, h = 20000, 0.1
+    out, *_ = oracle.solve("crn", "em", np.tile(y[:, None], (1, N)), np.tile(np.array(CRN_P)[:, None], (1, N)),
+                           (0, h), h, seed=11)
+    d = out[0] - y[:, None]
+    H = 1 / 3
+    mean = h * oracle.rhs("crn", y, CRN_P)
+    var = h * eta**2 * np.array([nu0 + H + y[0], (y[0] + y[1]) / tau, (y[1] + y[2]) / tau, (y[2] + y[3]) / tau])
+    se_m = np.sqrt(var / N)
+    assert np.all(np.abs(d.mean(1) - mean) < 5 * se_m)
+    assert np.all(np.abs(d.var(1, ddof=1) / var - 1) < 5 * np.sqrt(2 / N))
+    # nw = 8 normals per step: four independent Box–Muller pairs
+    z = oracle.normals(3, 7, 0, 20000, "f64", nw=8)
+    assert np.abs(np.corrcoef(z.T) - np.eye(8)).max() < 0.04
