@@ -267,7 +267,8 @@ def test_paired_fp32_kernels_ragged(N):
     np.testing.assert_array_equal(rc, orc)
     np.testing.assert_array_equal(na, ona)
     ok = rc == 0
-    assert traj_relerr(g[..., ok], o[..., ok]).max() <= TOL_FIXED["f32"]
+    if ok.any():
+        assert traj_relerr(g[..., ok], o[..., ok]).max() <= TOL_FIXED["f32"]
     np.testing.assert_array_equal(g[..., ~ok], o[..., ~ok])     # diverged lane keeps u0
 
 
