@@ -65,7 +65,10 @@ typedef enum {
   ENS_GBM = 4,             /* n=3, m=2 p=(r,V), dX = rX dt + VX dW */
   ENS_EXPDECAY = 5,        /* n=1, m=1 u' = −λu (closed-form test model) */
   ENS_HARMONIC = 6,        /* n=2, m=1 x' = v, v' = −ω²x (closed-form test model) */
-  ENS_CRN = 7              /* n=4, m=6 p=(S,D,τ,ν0,n,η), 8 Wiener: σ-factor CRN SDE, P:690-725 (DESIGN R14) */
+  ENS_CRN = 7,             /* n=4, m=6 p=(S,D,τ,ν0,n,η), 8 Wiener: σ-factor CRN SDE, P:690-725 (DESIGN R14) */
+  ENS_OREGO = 8,           /* n=3,  m=3  stiff Oregonator, P:739-749 (AD Jacobian, DESIGN R15) */
+  ENS_HIRES = 9,           /* n=8,  m=12 stiff HIRES, P:751-776 (AD Jacobian) */
+  ENS_POLLU = 10           /* n=20, m=25 stiff POLLU, P:779-833 (AD Jacobian; Rosenbrock23 only) */
 } ens_model;
 
 typedef enum {

@@ -33,10 +33,12 @@
 
 namespace orc {
 
+constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m = 25)
+
 // ---------------------------------------------------------------- enums ----
 // Numbering mirrors include/ens.h (an interface fact, not shared code).
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
-             GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7 };
+             GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10 };
 enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
@@ -51,6 +53,9 @@ static bool dims(int model, Dims* d) {
     case EXPDECAY:       *d = {1, 1, 0, false}; return true;   // test model (closed form)
     case HARMONIC:       *d = {2, 1, 0, false}; return true;   // test model (closed form)
     case CRN:            *d = {4, 6, 8, true};  return true;   // P:690-725 (σ-factor CRN, 8 Wiener)
+    case OREGO:          *d = {3, 3, 0, false}; return true;
+    case HIRES:          *d = {8, 12, 0, false}; return true;
+    case POLLU:          *d = {20, 25, 0, false}; return true;
   }
   return false;
 }
@@ -76,6 +81,99 @@ template <class T> static CrnTerms<T> crn_terms(const T* y, const T* p) {
   c.hill = a / ((a + b) + T(1));
   c.itau = T(1) / p[2];
   return c;
+}
+
+// ------------------------------------------------ forward-mode AD (R15) ----
+// Dual number with N partials (P:329 forward-mode AD for the Rosenbrock
+// Jacobian). Operation order per DESIGN §4: (a·b)' = fma(a, b', a'·b); a scalar
+// operand (constant or parameter) has no partials.
+template <class T, int N> struct Dual { T v; T d[N]; };
+template <class T, int N> static Dual<T, N> operator+(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v + b.v; for (int k = 0; k < N; ++k) r.d[k] = a.d[k] + b.d[k]; return r;
+}
+template <class T, int N> static Dual<T, N> operator-(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v - b.v; for (int k = 0; k < N; ++k) r.d[k] = a.d[k] - b.d[k]; return r;
+}
+template <class T, int N> static Dual<T, N> operator-(const Dual<T, N>& a) {
+  Dual<T, N> r; r.v = -a.v; for (int k = 0; k < N; ++k) r.d[k] = -a.d[k]; return r;
+}
+template <class T, int N> static Dual<T, N> operator*(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v * b.v; for (int k = 0; k < N; ++k) r.d[k] = std::fma(a.v, b.d[k], a.d[k] * b.v); return r;
+}
+template <class T, int N> static Dual<T, N> operator*(T s, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = s * b.v; for (int k = 0; k < N; ++k) r.d[k] = s * b.d[k]; return r;
+}
+template <class T, int N> static Dual<T, N> operator/(const Dual<T, N>& a, T s) {
+  Dual<T, N> r; r.v = a.v / s; for (int k = 0; k < N; ++k) r.d[k] = a.d[k] / s; return r;
+}
+template <class T, int N> static Dual<T, N> operator+(T s, const Dual<T, N>& b) {
+  Dual<T, N> r = b; r.v = s + b.v; return r;
+}
+template <class T, int N> static Dual<T, N> operator+(const Dual<T, N>& a, T s) {
+  Dual<T, N> r = a; r.v = a.v + s; return r;
+}
+template <class T, int N> static Dual<T, N> operator-(T s, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = s - b.v; for (int k = 0; k < N; ++k) r.d[k] = -b.d[k]; return r;
+}
+
+// The stiff test suite, written over a value type Y (T or Dual)
+// with parameters T, terms evaluated left to right as printed.
+template <class Y, class T> static void rhs_stiff(int model, const Y* y, const T* p, Y* o) {
+  if (model == OREGO) {        // p = (k1, k2, k3); R16: dy1 = +k1(…) (the printed − is a typo)
+    const Y inner = (T(1) - p[1] * y[0]) - y[1];
+    o[0] = p[0] * (y[1] + y[0] * inner);
+    o[1] = (y[2] - (T(1) + y[0]) * y[1]) / p[0];
+    o[2] = p[2] * (y[0] - y[2]);
+  } else if (model == HIRES) { // p = (1.71, 0.43, 8.32, 0.0007, 8.75, 10.03, 0.035, 1.12, 1.745, 280, 0.69, 1.81)
+    o[0] = ((-(p[0] * y[0]) + p[1] * y[1]) + p[2] * y[2]) + p[3];
+    o[1] = p[0] * y[0] - p[4] * y[1];
+    o[2] = (-(p[5] * y[2]) + p[1] * y[3]) + p[6] * y[4];
+    o[3] = (p[2] * y[1] + p[0] * y[2]) - p[7] * y[3];
+    o[4] = (-(p[8] * y[4]) + p[1] * y[5]) + p[1] * y[6];
+    const Y r = (p[9] * y[5]) * y[7];
+    o[5] = (((-r + p[10] * y[3]) + p[0] * y[4]) - p[1] * y[5]) + p[10] * y[6];
+    o[6] = r - p[11] * y[6];
+    o[7] = -r + p[11] * y[6];
+  } else {                     // POLLU, P:782-825 (u9, u16 read as y9, y16): reaction rates r1..r25
+    const T* k = p;
+    const Y r1 = k[0] * y[0], r2 = (k[1] * y[1]) * y[3], r3 = (k[2] * y[4]) * y[1], r4 = k[3] * y[6];
+    const Y r5 = k[4] * y[6], r6 = (k[5] * y[6]) * y[5], r7 = k[6] * y[8], r8 = (k[7] * y[8]) * y[5];
+    const Y r9 = (k[8] * y[10]) * y[1], r10 = (k[9] * y[10]) * y[0], r11 = k[10] * y[12];
+    const Y r12 = (k[11] * y[9]) * y[1], r13 = k[12] * y[13], r14 = (k[13] * y[0]) * y[5], r15 = k[14] * y[2];
+    const Y r16 = k[15] * y[3], r17 = k[16] * y[3], r18 = k[17] * y[15], r19 = k[18] * y[15];
+    const Y r20 = (k[19] * y[16]) * y[5], r21 = k[20] * y[18], r22 = k[21] * y[18], r23 = (k[22] * y[0]) * y[3];
+    const Y r24 = (k[23] * y[18]) * y[0], r25 = k[24] * y[19];
+    o[0] = (((((((((((-r1 - r10) - r14) - r23) - r24) + r2) + r3) + r9) + r11) + r12) + r22) + r25);
+    o[1] = ((((-r2 - r3) - r9) - r12) + r1) + r21;
+    o[2] = (((-r15 + r1) + r17) + r19) + r22;
+    o[3] = (((-r2 - r16) - r17) - r23) + r15;
+    o[4] = ((((-r3 + T(2) * r4) + r6) + r7) + r13) + r20;
+    o[5] = ((((-r6 - r8) - r14) - r20) + r3) + T(2) * r18;
+    o[6] = ((-r4 - r5) - r6) + r13;
+    o[7] = ((r4 + r5) + r6) + r7;
+    o[8] = -r7 - r8;
+    o[9] = (-r12 + r7) + r9;
+    o[10] = ((-r9 - r10) + r8) + r11;
+    o[11] = r9;
+    o[12] = -r11 + r10;
+    o[13] = -r13 + r12;
+    o[14] = r14;
+    o[15] = (-r18 - r19) + r16;
+    o[16] = -r20;
+    o[17] = r20;
+    o[18] = ((((-r21 - r22) - r24) + r23) + r25);
+    o[19] = -r25 + r24;
+  }
+}
+template <class T, int N> static void ad_jac(int model, const T* u, const T* p, T* J) {
+  Dual<T, N> y[N], o[N];
+  for (int i = 0; i < N; ++i) {
+    y[i].v = u[i];
+    for (int k = 0; k < N; ++k) y[i].d[k] = (i == k) ? T(1) : T(0);
+  }
+  rhs_stiff<Dual<T, N>, T>(model, y, p, o);
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < N; ++k) J[i * N + k] = o[i].d[k];
 }
 
 // --------------------------------------------------------------- models ----
@@ -110,6 +208,7 @@ static void rhs(int model, const T* y, const T* p, T /*t*/, T* f) {
     }
     case EXPDECAY: f[0] = (-p[0]) * y[0]; return;          // u' = −λu
     case HARMONIC: f[0] = y[1]; f[1] = -(p[0] * y[0]); return;  // x' = v, v' = −ω² x
+    case OREGO: case HIRES: case POLLU: rhs_stiff<T, T>(model, y, p, f); return;
     case CRN: {
       // P:692-705 drift, p = (S, D, τ, ν0, n, η), y = ([σ], [A1], [A2], [A3])
       const CrnTerms<T> c = crn_terms<T>(y, p);
@@ -140,7 +239,7 @@ static void noise_update(int model, const T* y, const T* p, T t, const T* dW, T*
   if (model == CRN) {
     const CrnTerms<T> c = crn_terms<T>(y, p);
     const T eta = p[5];
-    T G[8];
+    T G[NMAX];
     G[0] = eta * std::sqrt(std::fmax(p[3] + c.hill, T(0)));
     G[1] = -(eta * std::sqrt(c.sp));
     const T r1 = eta * std::sqrt(c.sp * c.itau), r2 = eta * std::sqrt(std::fmax(y[1], T(0)) * c.itau);
@@ -152,7 +251,7 @@ static void noise_update(int model, const T* y, const T* p, T t, const T* dW, T*
     }
     return;
   }
-  T b[8];
+  T b[NMAX];
   diffusion<T>(model, y, p, t, b);
   for (int j = 0; j < 3; ++j) x[j] = std::fma(b[j], dW[j], x[j]);
 }
@@ -180,6 +279,9 @@ static void jac(int model, const T* y, const T* p, T /*t*/, T* J) {
     }
     case EXPDECAY: J[0] = -p[0]; return;
     case HARMONIC: J[0] = T(0); J[1] = T(1); J[2] = -p[0]; J[3] = T(0); return;
+    case OREGO: ad_jac<T, 3>(model, y, p, J); return;     // forward-mode AD (R15)
+    case HIRES: ad_jac<T, 8>(model, y, p, J); return;
+    case POLLU: ad_jac<T, 20>(model, y, p, J); return;
   }
 }
 
@@ -374,7 +476,7 @@ template <class T> static bool finite_vec(const T* v, int n) {
 // Per-trajectory problem + outputs (one column of the paper's U / P).
 template <class T> struct Traj {
   int n, m;
-  T u0[8], p[8];
+  T u0[NMAX], p[NMAX];
   uint64_t gidx;                 // global trajectory index (Philox counter)
   // outputs
   T* save;                       // [k][n] row-major for this trajectory (k = nsave) or [n] final
@@ -397,8 +499,8 @@ struct Opts {
 // Canonical order (DESIGN R1, §4): the step size multiplies each coefficient,
 // h·a_ij rounded to T; y = u; y = fma(h·a_ij, k_j, y) for j = 1..i−1.
 template <class T>
-static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7][8], T* unew, T* E) {
-  T y[8];
+static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7][NMAX], T* unew, T* E) {
+  T y[NMAX];
   for (int i = 1; i < 7; ++i) {
     for (int j = 0; j < n; ++j) {
       T acc = u[j];
@@ -420,7 +522,7 @@ static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7
 
 // Tsit5 free interpolant at θ ∈ (0,1) (DESIGN §4 order).
 template <class T>
-static void tsit5_interp(int n, T theta, T h, const T* u, T K[7][8], T* out) {
+static void tsit5_interp(int n, T theta, T h, const T* u, T K[7][NMAX], T* out) {
   T bt[7];
   bt[0] = std::fma(theta, std::fma(theta, std::fma(theta, (T)TS_R[0][3], (T)TS_R[0][2]), (T)TS_R[0][1]),
                    (T)TS_R[0][0]) * theta;
@@ -487,7 +589,7 @@ template <class T> static T pi_reject(const Ctrl& C, T h, T q2) {
 template <class T>
 static void solve_tsit5(const Opts& o, Traj<T>& tr) {
   const int n = tr.n, model = o.model;
-  T u[8], K[7][8], unew[8], E[8];
+  T u[NMAX], K[7][NMAX], unew[NMAX], E[NMAX];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
   const int k = o.k;
@@ -514,7 +616,7 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
       const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
       while (js < k && tau[js] <= tn) {
         if (tau[js] == tn) put(tr.save, n, js, unew);
-        else { T out[8]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
+        else { T out[NMAX]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
         ++js;
       }
       for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
@@ -540,7 +642,7 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
         const T tn = last ? tf : t + h;
         while (js < k && tau[js] <= tn) {
           if (tau[js] == tn) put(tr.save, n, js, unew);
-          else { T out[8]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
+          else { T out[NMAX]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
           ++js;
         }
         t = tn;
@@ -557,7 +659,7 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
   if (k == 0) put(tr.save, n, 0, u);
   else {
     const T nan = std::numeric_limits<T>::quiet_NaN();
-    T nv[8]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    T nv[NMAX]; for (int j = 0; j < n; ++j) nv[j] = nan;
     for (; js < k; ++js) put(tr.save, n, js, nv);   // unreached save points (DESIGN R6)
   }
 }
@@ -590,7 +692,7 @@ static bool lu_factor(int n, T* A, int* piv, T* inv) {
 }
 template <class T>
 static void lu_solve(int n, const T* LU, const int* piv, const T* inv, const T* b, T* x) {
-  T z[8];
+  T z[NMAX];
   for (int i = 0; i < n; ++i) z[i] = b[i];
   for (int kk = 0; kk < n; ++kk) if (piv[kk] != kk) std::swap(z[kk], z[piv[kk]]);
   for (int i = 0; i < n; ++i) {            // forward: unit lower
@@ -612,13 +714,13 @@ template <class T>
 static bool ros23_step(int model, int n, const T* p, T t, T h, const T* u, const T* F0,
                        T* unew, T* F2, T* k1, T* k2, T* E) {
   const T d = (T)R23_D, e32 = (T)R23_E32;
-  T J[64], W[64], inv[8]; int piv[8];
+  T J[NMAX * NMAX], W[NMAX * NMAX], inv[NMAX]; int piv[NMAX];
   jac<T>(model, u, p, t, J);
   const T hd = h * d;
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) W[i * n + j] = (i == j ? T(1) : T(0)) - hd * J[i * n + j];  // W = I − h d J
   if (!lu_factor<T>(n, W, piv, inv)) return false;
-  T rhsv[8], y[8], F1[8], k3[8];
+  T rhsv[NMAX], y[NMAX], F1[NMAX], k3[NMAX];
   lu_solve<T>(n, W, piv, inv, F0, k1);                                  // k1 = W⁻¹ F0
   const T hh = h * T(0.5);
   for (int j = 0; j < n; ++j) y[j] = std::fma(hh, k1[j], u[j]);        // u + h/2 k1
@@ -659,7 +761,7 @@ template <class T>
 static void solve_ros23(const Opts& o, Traj<T>& tr) {
   const int n = tr.n, model = o.model;
   const Ctrl& C = CTRL_ROS23;
-  T u[8], F0[8], unew[8], F2[8], k1[8], k2[8], E[8];
+  T u[NMAX], F0[NMAX], unew[NMAX], F2[NMAX], k1[NMAX], k2[NMAX], E[NMAX];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
   const int k = o.k;
@@ -686,7 +788,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
       const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
       while (js < k && tau[js] <= tn) {
         if (tau[js] == tn) put(tr.save, n, js, unew);
-        else { T out[8]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
+        else { T out[NMAX]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
         ++js;
       }
       for (int j = 0; j < n; ++j) { u[j] = unew[j]; F0[j] = F2[j]; }
@@ -714,7 +816,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
         const T tn = last ? tf : t + h;
         while (js < k && tau[js] <= tn) {
           if (tau[js] == tn) put(tr.save, n, js, unew);
-          else { T out[8]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
+          else { T out[NMAX]; ros23_interp<T>(n, (tau[js] - t) / h, h, u, k1, k2, out); put(tr.save, n, js, out); }
           ++js;
         }
         t = tn;
@@ -731,7 +833,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
   if (k == 0) put(tr.save, n, 0, u);
   else {
     const T nan = std::numeric_limits<T>::quiet_NaN();
-    T nv[8]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    T nv[NMAX]; for (int j = 0; j < n; ++j) nv[j] = nan;
     for (; js < k; ++js) put(tr.save, n, js, nv);
   }
 }
@@ -745,7 +847,7 @@ static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   Dims d;
   dims(model, &d);
   const int nw = d.nw;
-  T u[8], a[8], x[8], z[8], dW[8];
+  T u[NMAX], a[NMAX], x[NMAX], z[NMAX], dW[NMAX];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
   int64_t nsteps; double h_last;
@@ -897,13 +999,13 @@ void orc_fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_
 
 // LU pins: factor + solve one system (row-major A, n ≤ 8). Returns 0 ok, 1 singular.
 int orc_lu_solve(int dtype, int n, const void* A, const void* b, void* x) {
-  int piv[8];
+  int piv[orc::NMAX];
   if (dtype == 0) {
-    float W[64], inv[8]; std::memcpy(W, A, sizeof(float) * n * n);
+    float W[orc::NMAX * orc::NMAX], inv[orc::NMAX]; std::memcpy(W, A, sizeof(float) * n * n);
     if (!orc::lu_factor<float>(n, W, piv, inv)) return 1;
     orc::lu_solve<float>(n, W, piv, inv, (const float*)b, (float*)x);
   } else {
-    double W[64], inv[8]; std::memcpy(W, A, sizeof(double) * n * n);
+    double W[orc::NMAX * orc::NMAX], inv[orc::NMAX]; std::memcpy(W, A, sizeof(double) * n * n);
     if (!orc::lu_factor<double>(n, W, piv, inv)) return 1;
     orc::lu_solve<double>(n, W, piv, inv, (const double*)b, (double*)x);
   }

@@ -14,6 +14,7 @@
 #include "em.cuh"
 #include "inputs.cuh"
 #include "models.cuh"
+#include "models_stiff.cuh"
 #include "ros23.cuh"
 #include "sched.cuh"
 #include "stats.cuh"
@@ -34,6 +35,9 @@ bool model_dims(int model, int* n, int* m, int* nw) {
     case ENS_EXPDECAY: *n = 1; *m = 1; *nw = 0; return true;
     case ENS_HARMONIC: *n = 2; *m = 1; *nw = 0; return true;
     case ENS_CRN: *n = 4; *m = 6; *nw = 8; return true;
+    case ENS_OREGO: *n = 3; *m = 3; *nw = 0; return true;
+    case ENS_HIRES: *n = 8; *m = 12; *nw = 0; return true;
+    case ENS_POLLU: *n = 20; *m = 25; *nw = 0; return true;
   }
   return false;
 }
@@ -97,7 +101,13 @@ template <class M, class T>
 ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
   const dim3 g = grid_for<T>(a.N), b(kBlock);
+  if constexpr (M::n > 8) {
+    // POLLU (n = 20) is built for its stiff solver only (register-resident Tsit5 stages for
+    // n = 20 are not instantiated)
+    if (alg == ENS_TSIT5) return ENS_E_UNSUPPORTED;
+  }
   if (alg == ENS_TSIT5) {
+   if constexpr (M::n <= 8) {
     if (!opt->adaptive) {
       if constexpr (std::is_same<T, float>::value) {
         // fp32: two trajectories per thread on the packed FFMA2 path
@@ -130,6 +140,7 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       if (save) adaptive_static_kernel<Tsit5Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
       else adaptive_static_kernel<Tsit5Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
     }
+   }
   } else {  // Rosenbrock23
     if (!opt->adaptive) {
       if (save) ros23_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
@@ -185,6 +196,11 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(a, opt, s);
     case ENS_GBM: return run_sde<GBM, T>(a, opt, s);
     case ENS_CRN: return run_sde<CRN, T>(a, opt, s);
+    case ENS_OREGO: return run_ode<Orego, T>(alg, a, opt, s);
+    case ENS_HIRES: return run_ode<Hires, T>(alg, a, opt, s);
+    case ENS_POLLU:   // fp64 only (20 × 21 dual numbers per AD Jacobian: the fp32 build is not worth its size)
+      if constexpr (sizeof(T) == 8) return run_ode<Pollu, T>(alg, a, opt, s);
+      else return ENS_E_UNSUPPORTED;
   }
   return ENS_E_INVALID_ARG;
 }
@@ -414,12 +430,26 @@ ens_status ens_generate_inputs(ens_model model, ens_dtype dtype, ens_recipe reci
   if (recipe < ENS_RECIPE_RANDOM10 || recipe > ENS_RECIPE_GRID) return ENS_E_INVALID_ARG;
   if (recipe == ENS_RECIPE_RHO_SWEEP && model != ENS_LORENZ) return ENS_E_UNSUPPORTED;
   if ((recipe == ENS_RECIPE_GRID) != (model == ENS_CRN)) return ENS_E_UNSUPPORTED;
-  // p̄ and ū0 of DESIGN §6 (same table as synth/inputs.py)
   // p̄ and ū0 of DESIGN §6 (same table as synth/inputs.py); CRN: Table-5 ranges (lo, hi)
   static const double PB[7][4] = {{10.0, 28.0, 8.0 / 3.0, 0}, {0.04, 3e7, 1e4, 0}, {10.0, 28.0, 8.0 / 3.0, 0.1},
                                   {10.0, 28.0, 8.0 / 3.0, 0.1}, {1.5, 0.01, 0, 0}, {1.0, 0, 0, 0}, {1.0, 0, 0, 0}};
   static const double UB[7][3] = {{1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {1, 0, 0}, {0.1, 0.1, 0.1}, {1, 0, 0}, {1, 0, 0}};
   static const double CRN_LO[6] = {0.1, 0.1, 0.1, 0.01, 2.0, 0.001}, CRN_HI[6] = {100.0, 100.0, 100.0, 0.2, 4.0, 0.1};
+  // stiff suite: rate constants and initial states as printed
+  static const double OREGO_P[3] = {77.27, 8.375e-6, 0.161}, OREGO_U[3] = {1.0, 2.0, 3.0};
+  static const double HIRES_P[12] = {1.71, 0.43, 8.32, 0.0007, 8.75, 10.03, 0.035, 1.12, 1.745, 280.0, 0.69, 1.81};
+  static const double HIRES_U[8] = {1.0, 0, 0, 0, 0, 0, 0, 0.0057};
+  static const double POLLU_P[25] = {0.35, 26.6, 12300.0, 0.00086, 0.00082, 15000.0, 0.00013, 24000.0, 16500.0,
+                                     9000.0, 0.022, 12000.0, 1.88, 16300.0, 4.8e6, 0.00035, 0.0175, 1.0e8, 4.44e11,
+                                     1240.0, 2.1, 5.78, 0.0474, 1780.0, 3.12};
+  static const double POLLU_U[20] = {0.0, 0.2, 0.0, 0.04, 0.0, 0.0, 0.1, 0.3, 0.017, 0.0,
+                                     0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.007, 0.0, 0.0, 0.0};
+  if (model >= ENS_OREGO) {
+    const double* pb = model == ENS_OREGO ? OREGO_P : model == ENS_HIRES ? HIRES_P : POLLU_P;
+    const double* ub = model == ENS_OREGO ? OREGO_U : model == ENS_HIRES ? HIRES_U : POLLU_U;
+    for (int j = 0; j < sp.m; ++j) sp.pbar[j] = pb[j];
+    for (int j = 0; j < sp.n; ++j) sp.ubar[j] = ub[j];
+  } else
   if (model == ENS_CRN) {
     for (int j = 0; j < 6; ++j) { sp.lo[j] = CRN_LO[j]; sp.hi[j] = CRN_HI[j]; }
     const int64_t nt = N_total > 0 ? N_total : N;

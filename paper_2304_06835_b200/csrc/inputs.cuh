@@ -20,7 +20,7 @@ __device__ __forceinline__ double input_uniform(uint64_t seed, uint64_t g, int j
 
 struct InputSpec {
   int n, m, recipe;
-  double pbar[8], ubar[8];
+  double pbar[32], ubar[32];
   double n_total;
   double lo[8], hi[8];   // grid recipe ranges
   int64_t levels;        // grid recipe levels per parameter

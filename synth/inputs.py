@@ -38,6 +38,15 @@ MODELS = {
                            lo=(0.1, 0.1, 0.1, 0.01, 2.0, 0.001), hi=(100.0, 100.0, 100.0, 0.2, 4.0, 0.1)),
 }
 RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
+# stiff test suite, constants and initial states as printed
+MODELS["orego"] = dict(pbar=(77.27, 8.375e-6, 0.161), u0=(1.0, 2.0, 3.0))
+MODELS["hires"] = dict(pbar=(1.71, 0.43, 8.32, 0.0007, 8.75, 10.03, 0.035, 1.12, 1.745, 280.0, 0.69, 1.81),
+                       u0=(1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0057))
+MODELS["pollu"] = dict(pbar=(0.35, 26.6, 12300.0, 0.00086, 0.00082, 15000.0, 0.00013, 24000.0, 16500.0, 9000.0,
+                             0.022, 12000.0, 1.88, 16300.0, 4.8e6, 0.00035, 0.0175, 1.0e8, 4.44e11, 1240.0, 2.1,
+                             5.78, 0.0474, 1780.0, 3.12),
+                       u0=(0.0, 0.2, 0.0, 0.04, 0.0, 0.0, 0.1, 0.3, 0.017, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0,
+                           0.007, 0.0, 0.0, 0.0))
 
 
 def grid_levels(n_total: int, m: int = 6) -> int:

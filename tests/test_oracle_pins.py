@@ -573,3 +573,53 @@ def test_crn_one_step_noise_variance():
     # nw = 8 normals per step: four independent Box–Muller pairs
     z = oracle.normals(3, 7, 0, 20000, "f64", nw=8)
     assert np.abs(np.corrcoef(z.T) - np.eye(8)).max() < 0.04
+
+
+# ------------------------------------------------- stiff suite (NEXT-4) --
+def test_stiff_suite_literature_references():
+    """P:733-844 OREGO / HIRES / POLLU with Rosenbrock23 and the forward-mode AD
+    Jacobian (R15) against the IVP test-set reference solutions."""
+    from synth.inputs import make_inputs
+    g = gold("stiff_references.json")
+    for model, tol, bound in [("hires", 1e-10, 2e-6), ("pollu", 1e-10, 1e-6), ("orego", 1e-8, 1e-4)]:
+        u0, p = make_inputs(model, "const", 1)
+        if model == "pollu":
+            u0[8, 0] = g["pollu"]["y9_0"]
+        out, rc, na, nr = oracle.solve(model, "rosenbrock23", u0, p, (0, g[model]["tf"]), 1e-6, adaptive=True,
+                                       abstol=tol, reltol=tol, p_broadcast=True)
+        assert rc[0] == 0
+        ref = np.array(g[model]["y"])
+        big = np.abs(ref) > 1e-10
+        rel = np.abs(out[0, :, 0] - ref)[big] / np.abs(ref[big])
+        assert rel.max() < bound, (model, rel.max())
+
+
+def test_hires_linear_invariant():
+    """HIRES: d(y7 + y8)/dt = 0 exactly; an exact-Jacobian Rosenbrock
+    method preserves the linear invariant y7 + y8 = 0.0057 to rounding."""
+    from synth.inputs import make_inputs
+    u0, p = make_inputs("hires", "random10", 3, seed=5)
+    sa = np.linspace(0, 321.8122, 50)
+    out, rc, *_ = oracle.solve("hires", "rosenbrock23", u0, p, (0, 321.8122), 1e-6, adaptive=True, abstol=1e-8,
+                               reltol=1e-8, saveat=sa)
+    assert (rc == 0).all()
+    assert np.abs(out[:, 6, :] + out[:, 7, :] - 0.0057).max() < 1e-15
+
+
+@pytest.mark.parametrize("model", ["orego", "hires", "pollu"])
+def test_ad_jacobian_vs_central_differences(model):
+    """Forward-mode AD Jacobian (R15) equals central finite differences."""
+    from synth.inputs import make_inputs
+    rng = np.random.default_rng(2)
+    u0, p = make_inputs(model, "random10", 4, seed=9)
+    n = u0.shape[0]
+    for i in range(4):
+        u = np.abs(u0[:, i]) + rng.uniform(0.01, 1.0, n) * (np.abs(u0[:, i]).max() + 0.1)
+        J = oracle.jac(model, u, p[:, i])
+        Jfd = np.zeros_like(J)
+        for j in range(n):
+            eps = 1e-6 * max(1.0, abs(u[j]))
+            up, um = u.copy(), u.copy()
+            up[j] += eps; um[j] -= eps
+            Jfd[:, j] = (oracle.rhs(model, up, p[:, i]) - oracle.rhs(model, um, p[:, i])) / (2 * eps)
+        np.testing.assert_allclose(J, Jfd, rtol=1e-5, atol=1e-6 * max(1.0, np.abs(J).max()))
