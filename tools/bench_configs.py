@@ -106,6 +106,15 @@ def main():
         for dt_ in ["f32", "f64"]:
             run("C4", model, "em", "const", 10**6, dt_, (0.0, 1.0), 1e-3, None, reps=3, seed=0xC4, saveat=sa4,
                 stats=True, store_states=False)
+    # NEXT-3: σ-factor CRN SDE, 10^6-point parameter grid, dt = 0.1 on [0, 1000], stats every 100
+    sa6 = [100.0 * j for j in range(11)]
+    for dt_ in ["f32", "f64"]:
+        run("CRN", "crn", "em", "grid", 10**6 if not args.quick else 10**5, dt_, (0.0, 1000.0), 0.1, None, reps=2,
+            seed=0xC7, saveat=sa6, stats=True, store_states=False)
+    # NEXT-4: stiff suite at the paper's 8192 trajectories, Rosenbrock23 fp64, tol 1e-8
+    for model, tf in [("orego", 30.0), ("hires", 321.8122), ("pollu", 60.0)]:
+        run("stiff-" + model, model, "rosenbrock23", "random10", 8192, "f64", (0.0, tf), 1e-6, "ros23", reps=3,
+            input_seed=0x57, adaptive=True, abstol=1e-8, reltol=1e-8)
     # C5: Lorenz fp32 10^8 on one GPU (the 8-GPU run shards this), random p ±10 %
     if not args.quick:
         run("C5-1gpu", "lorenz", "tsit5", "random10", 10**8, "f32", (0.0, 1.0), 1e-3, "tsit5_fixed", reps=2,
