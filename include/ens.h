@@ -68,7 +68,9 @@ typedef enum {
   ENS_CRN = 7,             /* n=4, m=6 p=(S,D,τ,ν0,n,η), 8 Wiener: σ-factor CRN SDE, P:690-725 (DESIGN R14) */
   ENS_OREGO = 8,           /* n=3,  m=3  stiff Oregonator, P:739-749 (AD Jacobian, DESIGN R15) */
   ENS_HIRES = 9,           /* n=8,  m=12 stiff HIRES, P:751-776 (AD Jacobian) */
-  ENS_POLLU = 10           /* n=20, m=25 stiff POLLU, P:779-833 (AD Jacobian; Rosenbrock23 only) */
+  ENS_POLLU = 10,          /* n=20, m=25 stiff POLLU, P:779-833 (AD Jacobian; Rosenbrock23 only) */
+  ENS_BALL = 11            /* n=2, m=2 p=(g,e) bouncing ball with an event (x crosses 0 ↓ → v ← −e v),
+                              P:514-524; adaptive Tsit5 only (DESIGN R18) */
 } ens_model;
 
 typedef enum {

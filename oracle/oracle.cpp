@@ -38,7 +38,8 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 // ---------------------------------------------------------------- enums ----
 // Numbering mirrors include/ens.h (an interface fact, not shared code).
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
-             GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10 };
+             GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
+             BALL = 11 };
 enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
@@ -56,6 +57,7 @@ static bool dims(int model, Dims* d) {
     case OREGO:          *d = {3, 3, 0, false}; return true;
     case HIRES:          *d = {8, 12, 0, false}; return true;
     case POLLU:          *d = {20, 25, 0, false}; return true;
+    case BALL:           *d = {2, 2, 0, false}; return true;   // P:644-665 bouncing ball (event)
   }
   return false;
 }
@@ -209,6 +211,7 @@ static void rhs(int model, const T* y, const T* p, T /*t*/, T* f) {
     case EXPDECAY: f[0] = (-p[0]) * y[0]; return;          // u' = −λu
     case HARMONIC: f[0] = y[1]; f[1] = -(p[0] * y[0]); return;  // x' = v, v' = −ω² x
     case OREGO: case HIRES: case POLLU: rhs_stiff<T, T>(model, y, p, f); return;
+    case BALL: f[0] = y[1]; f[1] = -p[0]; return;         // x' = v, v' = −g
     case CRN: {
       // P:692-705 drift, p = (S, D, τ, ν0, n, η), y = ([σ], [A1], [A2], [A3])
       const CrnTerms<T> c = crn_terms<T>(y, p);
@@ -282,6 +285,7 @@ static void jac(int model, const T* y, const T* p, T /*t*/, T* J) {
     case OREGO: ad_jac<T, 3>(model, y, p, J); return;     // forward-mode AD (R15)
     case HIRES: ad_jac<T, 8>(model, y, p, J); return;
     case POLLU: ad_jac<T, 20>(model, y, p, J); return;
+    case BALL: J[0] = T(0); J[1] = T(1); J[2] = T(0); J[3] = T(0); return;
   }
 }
 
@@ -491,6 +495,17 @@ struct Opts {
   const double* saveat; int k;
 };
 
+// ---------------------------------------------------------------- events ----
+// Bouncing ball (Listing "callbacks"): condition g(u) = u[1] (the
+// height x), affect v ← −e·v with p = (g, e) (DESIGN R18).
+static bool has_event(int model) { return model == BALL; }
+template <class T> static T event_g(int /*model*/, const T* u) { return u[0]; }
+template <class T> static void event_affect(int /*model*/, T* u, const T* p) { u[1] = -(p[1] * u[1]); }
+template <class T> struct BisectIters;
+template <> struct BisectIters<float> { static constexpr int value = 24; };
+template <> struct BisectIters<double> { static constexpr int value = 52; };
+constexpr int EVENT_PTS = 10;   // condition samples per accepted step (θ = j/10)
+
 // ---------------------------------------------------------------- Tsit5 ----
 // One Tsit5 step from (t,u,k1) with step h:
 //   y_i = u + Σ_{j<i} (h a_ij) k_j,  k_i = f(y_i, t + c_i h)   (i = 2..7)
@@ -639,14 +654,52 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
       if (q2 < T(1)) {                              // accept iff q < 1
-        const T tn = last ? tf : t + h;
+        T tn = last ? tf : t + h;
+        // Event (DESIGN R18): downward zero crossing of the condition
+        // inside the accepted step → locate it on the step's interpolant by a
+        // fixed number of bisections, end the step there, apply the affect.
+        bool event = false;
+        T ue[NMAX];
+        if (has_event(model)) {
+          // sample g at θ_j = j/M (j = 1..M, θ_M = 1 is the step end) so that a
+          // whole excursion inside one long step is still seen
+          T gprev = event_g<T>(model, u), thprev = T(0);
+          for (int j = 1; j <= EVENT_PTS && !event; ++j) {
+            const T th = (j == EVENT_PTS) ? T(1) : (T)j / (T)EVENT_PTS;
+            T xj[NMAX];
+            if (j == EVENT_PTS) { for (int c = 0; c < n; ++c) xj[c] = unew[c]; }
+            else tsit5_interp<T>(n, th, h, u, K, xj);
+            const T gj = event_g<T>(model, xj);
+            if (gprev > T(0) && gj <= T(0)) {
+              T lo = thprev, hi = th;
+              for (int it = 0; it < BisectIters<T>::value; ++it) {
+                const T mid = (lo + hi) * T(0.5);
+                T xm[NMAX];
+                tsit5_interp<T>(n, mid, h, u, K, xm);
+                if (event_g<T>(model, xm) > T(0)) lo = mid; else hi = mid;
+              }
+              if (hi == T(1)) { for (int c = 0; c < n; ++c) ue[c] = unew[c]; }
+              else tsit5_interp<T>(n, hi, h, u, K, ue);
+              tn = (hi == T(1)) ? tn : t + hi * h;
+              event = true;
+            }
+            gprev = gj; thprev = th;
+          }
+        }
+        const T* uend = event ? ue : unew;
         while (js < k && tau[js] <= tn) {
-          if (tau[js] == tn) put(tr.save, n, js, unew);
+          if (tau[js] == tn) put(tr.save, n, js, uend);
           else { T out[NMAX]; tsit5_interp<T>(n, (tau[js] - t) / h, h, u, K, out); put(tr.save, n, js, out); }
           ++js;
         }
         t = tn;
-        for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
+        if (event) {
+          event_affect<T>(model, ue, p);
+          for (int j = 0; j < n; ++j) u[j] = ue[j];
+          rhs<T>(model, u, p, t, K[0]);              // FSAL no longer valid after the affect
+        } else {
+          for (int j = 0; j < n; ++j) { u[j] = unew[j]; K[0][j] = K[6][j]; }
+        }
         tr.n_accept++;
         h = pi_accept<T>(C, h, q2, &lq_old);
       } else {

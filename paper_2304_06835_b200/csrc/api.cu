@@ -38,6 +38,7 @@ bool model_dims(int model, int* n, int* m, int* nw) {
     case ENS_OREGO: *n = 3; *m = 3; *nw = 0; return true;
     case ENS_HIRES: *n = 8; *m = 12; *nw = 0; return true;
     case ENS_POLLU: *n = 20; *m = 25; *nw = 0; return true;
+    case ENS_BALL: *n = 2; *m = 2; *nw = 0; return true;
   }
   return false;
 }
@@ -198,6 +199,7 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_CRN: return run_sde<CRN, T>(a, opt, s);
     case ENS_OREGO: return run_ode<Orego, T>(alg, a, opt, s);
     case ENS_HIRES: return run_ode<Hires, T>(alg, a, opt, s);
+    case ENS_BALL: return run_ode<Ball, T>(alg, a, opt, s);
     case ENS_POLLU:   // fp64 only (20 × 21 dual numbers per AD Jacobian: the fp32 build is not worth its size)
       if constexpr (sizeof(T) == 8) return run_ode<Pollu, T>(alg, a, opt, s);
       else return ENS_E_UNSUPPORTED;
@@ -215,6 +217,8 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
   const bool sde = nw > 0;
   if (sde != (alg == ENS_EM)) return ENS_E_ALG_MISMATCH;
+  // events (DESIGN R18) are located on the adaptive Tsit5 interpolant only
+  if (model == ENS_BALL && (alg != ENS_TSIT5 || !opt->adaptive)) return ENS_E_UNSUPPORTED;
   if (alg == ENS_EM && opt->adaptive) return ENS_E_ADAPTIVE_UNSUPPORTED;
   if (!std::isfinite(t0) || !std::isfinite(tf) || !std::isfinite(dt) || !(t0 < tf) || !(dt > 0))
     return ENS_E_BAD_TSPAN;
@@ -444,7 +448,10 @@ ens_status ens_generate_inputs(ens_model model, ens_dtype dtype, ens_recipe reci
                                      1240.0, 2.1, 5.78, 0.0474, 1780.0, 3.12};
   static const double POLLU_U[20] = {0.0, 0.2, 0.0, 0.04, 0.0, 0.0, 0.1, 0.3, 0.017, 0.0,
                                      0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.007, 0.0, 0.0, 0.0};
-  if (model >= ENS_OREGO) {
+  if (model == ENS_BALL) {   // g = 9.8, e = 0.85 (varies, R18); dropped from x = 50 at rest
+    sp.pbar[0] = 9.8; sp.pbar[1] = 0.85;
+    sp.ubar[0] = 50.0; sp.ubar[1] = 0.0;
+  } else if (model >= ENS_OREGO) {
     const double* pb = model == ENS_OREGO ? OREGO_P : model == ENS_HIRES ? HIRES_P : POLLU_P;
     const double* ub = model == ENS_OREGO ? OREGO_U : model == ENS_HIRES ? HIRES_U : POLLU_U;
     for (int j = 0; j < sp.m; ++j) sp.pbar[j] = pb[j];

@@ -127,6 +127,27 @@ struct CRN {
   }
 };
 
+// Bouncing ball with an event: x' = v, v' = −g; the
+// condition g(u) = x (u[1] in the paper's 1-based Listing) crossing zero
+// downward triggers the affect v ← −e·v; p = (g, e) (DESIGN R18).
+struct Ball {
+  static constexpr int n = 2, m = 2, nw = 0;
+  static constexpr bool has_event = true;
+  template <class T> __device__ __forceinline__ static void f(const T (&y)[2], const T (&p)[2], T, T (&o)[2]) {
+    o[0] = y[1];
+    o[1] = -p[0];
+  }
+  template <class T> __device__ __forceinline__ static void jac(const T (&)[2], const T (&)[2], T, T (&J)[2][2]) {
+    J[0][0] = T(0); J[0][1] = T(1); J[1][0] = T(0); J[1][1] = T(0);
+  }
+  template <class T> __device__ __forceinline__ static T event_g(const T (&y)[2]) { return y[0]; }
+  template <class T> __device__ __forceinline__ static void affect(T (&y)[2], const T (&p)[2]) {
+    y[1] = -(p[1] * y[1]);
+  }
+};
+template <class M, class = void> struct HasEvent { static constexpr bool value = false; };
+template <class M> struct HasEvent<M, decltype((void)M::has_event)> { static constexpr bool value = M::has_event; };
+
 template <class M, class T>
 __device__ __forceinline__ void apply_noise(const T (&y)[M::n], const T (&p)[M::m], T t, const T (&dW)[M::nw],
                                             T (&x)[M::n]) {

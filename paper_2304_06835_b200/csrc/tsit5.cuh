@@ -13,6 +13,7 @@
 // on the host, uniform registers in SASS); adaptive runs form them per step.
 #pragma once
 #include "common.cuh"
+#include "models.cuh"
 #include "vec2.cuh"
 
 namespace ens {
@@ -53,6 +54,8 @@ __host__ __device__ constexpr double ts_r(int i, int j) {
                               {0.0, 1.5, -4.0, 2.5}};
   return R[i][j];
 }
+constexpr int kEventPts = 10;   // event-condition samples per accepted step (DESIGN R18)
+
 // (i, l), 1 ≤ i ≤ 6, l < i  →  0..20
 __host__ __device__ constexpr int ts_idx(int i, int l) { return i * (i - 1) / 2 + l; }
 
@@ -301,15 +304,60 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     const T q2 = error_q2<n, T>(E, u, y, a.abstol, a.reltol);
     ++attempts;
     if (q2 < T(1)) {
-      const T tn = last ? a.tf : t + h;
+      T tn = last ? a.tf : t + h;
+      bool event = false;
+      if constexpr (HasEvent<M>::value) {
+        // DESIGN R18: sample the condition at θ_j = j/10 of the accepted step's
+        // interpolant; in the first downward-crossing bracket, a fixed number of
+        // bisections; the step ends at the crossing, where the affect applies.
+        T gprev = M::event_g(u), thprev = T(0);
+        for (int j = 1; j <= kEventPts && !event; ++j) {
+          const T th = (j == kEventPts) ? T(1) : (T)j / (T)kEventPts;
+          T xj[n];
+          if (j == kEventPts) {
+#pragma unroll
+            for (int c = 0; c < n; ++c) xj[c] = y[c];
+          } else {
+            tsit5_interp<n, T>(th, h, u, K, xj);
+          }
+          const T gj = M::event_g(xj);
+          if (gprev > T(0) && gj <= T(0)) {
+            T lo = thprev, hi = th;
+            for (int it = 0; it < (sizeof(T) == 4 ? 24 : 52); ++it) {
+              const T mid = (lo + hi) * T(0.5);
+              T xm[n];
+              tsit5_interp<n, T>(mid, h, u, K, xm);
+              if (M::event_g(xm) > T(0)) lo = mid; else hi = mid;
+            }
+            if (hi != T(1)) {
+              tsit5_interp<n, T>(hi, h, u, K, y);     // y ← state at the crossing
+              tn = t + hi * h;
+            }
+            event = true;
+          }
+          gprev = gj; thprev = th;
+        }
+      }
       if (SAVE) {
         const int64_t id[1] = {i};
         const bool lv[1] = {true};
         tsit5_save<n, T, T>(a, id, lv, js, t, tn, h, u, K, y);
       }
       t = tn;
+      if constexpr (HasEvent<M>::value) {
+        if (event) {
+          M::affect(y, par);
 #pragma unroll
-      for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
+          for (int j = 0; j < n; ++j) u[j] = y[j];
+          M::f(u, par, t, K[0]);                       // FSAL no longer valid after the affect
+        } else {
+#pragma unroll
+          for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
+      }
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, 7.0 / 50.0, 2.0 / 25.0);
     } else {

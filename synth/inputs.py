@@ -39,6 +39,8 @@ MODELS = {
 }
 RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
 # stiff test suite, constants and initial states as printed
+# bouncing ball: p = (g, e), dropped from rest at x = 50 (DESIGN R18)
+MODELS["ball"] = dict(pbar=(9.8, 0.85), u0=(50.0, 0.0))
 MODELS["orego"] = dict(pbar=(77.27, 8.375e-6, 0.161), u0=(1.0, 2.0, 3.0))
 MODELS["hires"] = dict(pbar=(1.71, 0.43, 8.32, 0.0007, 8.75, 10.03, 0.035, 1.12, 1.745, 280.0, 0.69, 1.81),
                        u0=(1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0057))
