@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--no-gather", action="store_true", help="skip the NCCL gather of final states (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-also", action="store_true", help="skip the fp64-fixed / adaptive side measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -252,6 +253,45 @@ def main():
     ms_max, k_max = t.tolist()
     assert (sol.retcode == 0).all().item(), "non-success retcodes in the benchmark ensemble"
 
+    # side measurements on the same N (metric names fp32 and fp64; adaptive is configs[1]'s other half)
+    also = {}
+    if not args.no_also:
+        def best_ms(fn, reps=3):
+            fn()
+            torch.cuda.synchronize(dev)
+            b = float("inf")
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                b = min(b, e0.elapsed_time(e1))
+            return b
+        other = torch.float64 if tdt == torch.float32 else torch.float32
+        u0o, po = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=other, index_offset=shard.index_offset,
+                                      N_total=N_total, device=dev)
+        msf = best_ms(lambda: ens.solve("lorenz", "tsit5", u0o, po, tspan, dt, stream=stream))
+        lanes_o = FP64_LANES_PER_SM if other == torch.float64 else FP32_LANES_PER_SM
+        pk_o = torch.cuda.get_device_properties(dev).multi_processor_count * lanes_o * 2 * SM_MAX_MHZ * 1e6
+        also["fixed_" + ("f64" if other == torch.float64 else "f32")] = {
+            "trajectories_per_s": N / (msf / 1e3), "kernel_ms": msf,
+            "frac_fp_peak": N * flops_per_traj(nsteps) / (msf / 1e3) / pk_o}
+        del u0o, po
+        sol_a = ens.Solution(u=torch.empty((3, N), dtype=tdt, device=dev),
+                             retcode=torch.empty(N, dtype=torch.int32, device=dev),
+                             n_accept=torch.empty(N, dtype=torch.int32, device=dev),
+                             n_reject=torch.empty(N, dtype=torch.int32, device=dev), stats=None)
+        msa = best_ms(lambda: ens.solve("lorenz", "tsit5", u0, p, tspan, dt, adaptive=True, abstol=1e-6,
+                                        reltol=1e-6, out=sol_a, stream=stream))
+        att = int((sol_a.n_accept.to(torch.int64) + sol_a.n_reject.to(torch.int64)).sum().item())
+        also["adaptive_" + args.dtype + "_tol1e-6"] = {
+            "trajectories_per_s": N / (msa / 1e3), "kernel_ms": msa, "attempted_steps_per_traj": att / N,
+            "frac_fp_peak_265flop_per_attempt": att * 265.0 / (msa / 1e3) / (
+                torch.cuda.get_device_properties(dev).multi_processor_count *
+                (FP32_LANES_PER_SM if tdt == torch.float32 else FP64_LANES_PER_SM) * 2 * SM_MAX_MHZ * 1e6)}
+        del sol_a
+
     # end to end through the C ABI on host buffers (pinned), copies in the timed region
     e2e = None
     if not args.no_e2e:
@@ -309,6 +349,7 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step[0] * args.steps,
             "e2e": e2e,
+            "also": also,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(N_total, dt, args.cpu_sample, os.cpu_count() or 1)

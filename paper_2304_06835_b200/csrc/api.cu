@@ -73,7 +73,8 @@ Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
   L.rows = std::max(1, k) * n;
   const bool stats = opt && opt->want_stats;
   L.nparts = 0;
-  if (stats) L.nparts = (alg == ENS_EM) ? cdiv(N, kBlock) : cdiv(N, kStatsChunk);
+  // EM: one partial per solver block; sized for the smallest block (32) so the layout is device independent
+  if (stats) L.nparts = (alg == ENS_EM) ? cdiv(N, 32) : cdiv(N, kStatsChunk);
   L.total = L.partial + align256((size_t)L.rows * (size_t)L.nparts * 3 * 8) + 256;
   return L;
 }
@@ -94,14 +95,22 @@ ens_status launch_check() {
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 
+// Block size of a one-thread-per-trajectory launch: 256 once the ensemble
+// fills every SM with 256-thread blocks, otherwise smaller (down to one warp)
+// so that small ensembles — C1's 1024 trajectories, the stiff suite's 8192 —
+// spread over all SMs instead of a handful (the latency-bound regime).
+int solver_block(int64_t threads) {
+  const int64_t per_sm = cdiv(threads, sm_count());
+  return (int)std::min<int64_t>(kBlock, std::max<int64_t>(32, cdiv(per_sm, 32) * 32));
+}
 template <class T>
-dim3 grid_for(int64_t N) { return dim3((unsigned)cdiv(N, kBlock)); }
+dim3 grid_for(int64_t N) { return dim3((unsigned)cdiv(N, solver_block(N))); }
 
 // ---------------------------------------------------------------- dispatch --
 template <class M, class T>
 ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
-  const dim3 g = grid_for<T>(a.N), b(kBlock);
+  const dim3 g = grid_for<T>(a.N), b(solver_block(a.N));
   if constexpr (M::n > 8) {
     // POLLU (n = 20) is built for its stiff solver only (register-resident Tsit5 stages for
     // n = 20 are not instantiated)
@@ -113,9 +122,10 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       if constexpr (std::is_same<T, float>::value) {
         // fp32: two trajectories per thread on the packed FFMA2 path
         const auto cf = make_tsit_coef<float, float2>(a.dt0, a.h_last);
-        const dim3 g2((unsigned)cdiv(a.N, 2 * kBlock));
-        if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b, 0, s>>>(a, cf);
-        else tsit5_fixed_kernel<M, f2, false><<<g2, b, 0, s>>>(a, cf);
+        const int64_t threads = cdiv(a.N, 2);
+        const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
+        if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b2, 0, s>>>(a, cf);
+        else tsit5_fixed_kernel<M, f2, false><<<g2, b2, 0, s>>>(a, cf);
       } else {
         const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
         if (save) tsit5_fixed_kernel<M, double, true><<<g, b, 0, s>>>(a, cf);
@@ -125,13 +135,13 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       int occ = 0;
       if (save) {
         auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, true>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
         kern<<<gr, b, 0, s>>>(a);
       } else {
         auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, false>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
         kern<<<gr, b, 0, s>>>(a);
       }
     } else {
@@ -150,13 +160,13 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       int occ = 0;
       if (save) {
         auto kern = adaptive_refill_kernel<Ros23Lane<M, T, true>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
         kern<<<gr, b, 0, s>>>(a);
       } else {
         auto kern = adaptive_refill_kernel<Ros23Lane<M, T, false>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, kBlock), (int64_t)std::max(1, occ) * sm_count()));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
+        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
         kern<<<gr, b, 0, s>>>(a);
       }
     } else {
@@ -180,7 +190,7 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
 
 template <class M, class T>
 ens_status run_sde(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
-  const dim3 g = grid_for<T>(a.N), b(kBlock);
+  const dim3 g = grid_for<T>(a.N), b(solver_block(a.N));
   if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
   else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
@@ -307,7 +317,8 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
       const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
       stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, kStatsChunk, a.partial);
     }
-    stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)L.nparts, out->stats);
+    const int64_t nparts = (alg == ENS_EM) ? (int64_t)grid_for<T>(N).x : L.nparts;
+    stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
     if (cudaPeekAtLastError() != cudaSuccess) return ENS_E_CUDA;
   }
   return ENS_OK;
