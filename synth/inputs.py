@@ -57,6 +57,8 @@ def grid_levels(n_total: int, m: int = 6) -> int:
     while L**m < n_total:
         L += 1
     return L
+
+
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
 
