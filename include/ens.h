@@ -76,7 +76,8 @@ typedef enum {
 typedef enum {
   ENS_TSIT5 = 0,           /* Tsitouras 5(4), FSAL, free 4th-order interpolant */
   ENS_ROSENBROCK23 = 1,    /* ode23s Rosenbrock-W 2(3), ode23s interpolant */
-  ENS_EM = 2               /* Euler–Maruyama, fixed step, diagonal noise */
+  ENS_EM = 2,              /* Euler–Maruyama, fixed step, diagonal or model-defined noise */
+  ENS_SIEA = 3             /* weak order 2.0 stochastic improved Euler, fixed step, diagonal noise (R19) */
 } ens_alg;
 
 typedef enum { ENS_F32 = 0, ENS_F64 = 1 } ens_dtype;

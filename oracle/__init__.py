@@ -24,7 +24,7 @@ _LIB = _HERE / "liboracle.so"
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
           "expdecay": 5, "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10,
           "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 

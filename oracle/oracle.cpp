@@ -40,7 +40,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -928,6 +928,59 @@ static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   if (k == 0) put(tr.save, n, 0, u);
 }
 
+// ------------------------------------------------ weak order 2 (SIEA) ----
+// GPUSIEA (weak order 2.0, stochastic improved Euler, diagonal noise);
+// the paper's SRK formulas are garbled, so DESIGN R19 takes the
+// Kloeden–Platen explicit weak order 2.0 scheme, component-wise for diagonal
+// noise with b_j = b_j(u_j):
+//   Ῡ = u + a h + b ΔW,  Υ± = u + a h ± b √h
+//   u ← u + ½(a(Ῡ) + a) h + ¼(b(Υ+) + b(Υ−) + 2b) ΔW + ¼(b(Υ+) − b(Υ−)) (ΔW² − h)/√h
+// Same Philox/Box–Muller noise stream as EM (ΔW = √h Z).
+template <class T>
+static void solve_siea(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+  const int n = tr.n, model = o.model;
+  T u[NMAX], a[NMAX], b[NMAX], z[NMAX], dW[NMAX], yb[NMAX], yp[NMAX], ym[NMAX], ab[NMAX], bp[NMAX], bm[NMAX];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  int64_t nsteps; double h_last;
+  fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+  const T hdt = (T)o.dt, hl = (T)h_last;
+  const T sq_dt = std::sqrt(hdt), sq_l = std::sqrt(hl);
+  const T isq_dt = T(1) / sq_dt, isq_l = T(1) / sq_l;
+  int js = 0;
+  const int k = o.k;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; }
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const bool last = (i == nsteps - 1);
+    const T h = last ? hl : hdt, sh = last ? sq_l : sq_dt, ish = last ? isq_l : isq_dt;
+    const T t = (T)(o.t0 + (double)i * o.dt);
+    rhs<T>(model, u, p, t, a);
+    diffusion<T>(model, u, p, t, b);
+    normalsN<T>(o.seed, (uint64_t)i, tr.gidx, n, z);
+    for (int j = 0; j < n; ++j) {
+      dW[j] = sh * z[j];
+      const T base = std::fma(h, a[j], u[j]);              // u + a h
+      yb[j] = std::fma(b[j], dW[j], base);                  // Ῡ
+      yp[j] = std::fma(b[j], sh, base);                     // Υ+
+      ym[j] = std::fma(-b[j], sh, base);                    // Υ−
+    }
+    rhs<T>(model, yb, p, t + h, ab);
+    diffusion<T>(model, yp, p, t + h, bp);
+    diffusion<T>(model, ym, p, t + h, bm);
+    for (int j = 0; j < n; ++j) {
+      T x = std::fma(h, (ab[j] + a[j]) * T(0.5), u[j]);
+      x = std::fma(((bp[j] + bm[j]) + T(2) * b[j]) * T(0.25), dW[j], x);
+      x = std::fma((bp[j] - bm[j]) * T(0.25), std::fma(dW[j], dW[j], -h) * ish, x);
+      u[j] = x;
+    }
+    tr.n_accept++;
+    while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
+  }
+  if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  if (k == 0) put(tr.save, n, 0, u);
+}
+
 // ------------------------------------------------------------- driver ----
 // Solves trajectories one after another (the plain loop of CS-6). Inputs and
 // outputs use the SoA layout of include/ens.h (component-major, trajectory
@@ -940,7 +993,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM) {
+  if (o.alg == EM || o.alg == SIEA) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
@@ -958,6 +1011,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     tr.save = buf.data();
     if (o.alg == TSIT5) solve_tsit5<T>(o, tr);
     else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
+    else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
     for (int s = 0; s < kk; ++s)
       for (int j = 0; j < n; ++j) u_out[((size_t)s * n + j) * N + i] = buf[(size_t)s * n + j];

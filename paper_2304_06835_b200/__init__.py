@@ -22,7 +22,7 @@ _LIB_PATH = _PKG / "libens.so"
 
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4, "expdecay": 5,
           "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10, "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3}
 DTYPES = {torch.float32: 0, torch.float64: 1}
 RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
 RETCODES = {0: "Success", 1: "MaxIters", 2: "DtLessThanMin", 3: "Diverged", 4: "Singular"}
@@ -181,7 +181,7 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
     dev = u0.device
     if out is None:
         shape = (k, n, N) if k else (n, N)
-        u_out = torch.empty(shape, dtype=u0.dtype, device=dev) if (store_states or alg != "em") else None
+        u_out = torch.empty(shape, dtype=u0.dtype, device=dev) if (store_states or alg not in ("em", "siea")) else None
         out = Solution(u=u_out, retcode=torch.empty(N, dtype=torch.int32, device=dev),
                        n_accept=torch.empty(N, dtype=torch.int32, device=dev),
                        n_reject=torch.empty(N, dtype=torch.int32, device=dev),

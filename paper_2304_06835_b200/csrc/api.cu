@@ -43,6 +43,7 @@ bool model_dims(int model, int* n, int* m, int* nw) {
   return false;
 }
 
+inline bool is_sde_alg(int alg) { return alg == ENS_EM || alg == ENS_SIEA; }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -74,7 +75,7 @@ Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
   const bool stats = opt && opt->want_stats;
   L.nparts = 0;
   // EM: one partial per solver block; sized for the smallest block (32) so the layout is device independent
-  if (stats) L.nparts = (alg == ENS_EM) ? cdiv(N, 32) : cdiv(N, kStatsChunk);
+  if (stats) L.nparts = is_sde_alg(alg) ? cdiv(N, 32) : cdiv(N, kStatsChunk);
   L.total = L.partial + align256((size_t)L.rows * (size_t)L.nparts * 3 * 8) + 256;
   return L;
 }
@@ -189,10 +190,19 @@ ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream
 }
 
 template <class M, class T>
-ens_status run_sde(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+ens_status run_sde(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const dim3 g = grid_for<T>(a.N), b(solver_block(a.N));
-  if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
-  else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+  if (alg == ENS_SIEA) {
+    if constexpr (M::nw == M::n) {   // diagonal noise only
+      if (opt->want_stats) em_kernel<M, T, true, true><<<g, b, 0, s>>>(a);
+      else em_kernel<M, T, false, true><<<g, b, 0, s>>>(a);
+    } else {
+      return ENS_E_UNSUPPORTED;
+    }
+  } else {
+    if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
+    else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 
@@ -203,10 +213,10 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_ROBERTSON: return run_ode<Robertson, T>(alg, a, opt, s);
     case ENS_EXPDECAY: return run_ode<ExpDecay, T>(alg, a, opt, s);
     case ENS_HARMONIC: return run_ode<Harmonic, T>(alg, a, opt, s);
-    case ENS_LORENZ_SDE_ADD: return run_sde<LorenzSDE<false>, T>(a, opt, s);
-    case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(a, opt, s);
-    case ENS_GBM: return run_sde<GBM, T>(a, opt, s);
-    case ENS_CRN: return run_sde<CRN, T>(a, opt, s);
+    case ENS_LORENZ_SDE_ADD: return run_sde<LorenzSDE<false>, T>(alg, a, opt, s);
+    case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(alg, a, opt, s);
+    case ENS_GBM: return run_sde<GBM, T>(alg, a, opt, s);
+    case ENS_CRN: return run_sde<CRN, T>(alg, a, opt, s);
     case ENS_OREGO: return run_ode<Orego, T>(alg, a, opt, s);
     case ENS_HIRES: return run_ode<Hires, T>(alg, a, opt, s);
     case ENS_BALL: return run_ode<Ball, T>(alg, a, opt, s);
@@ -222,14 +232,14 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
                     const ens_options* opt, int* n_out) {
   int n, m, nw;
   if (!opt || N < 1 || !model_dims(model, &n, &m, &nw)) return ENS_E_INVALID_ARG;
-  if (alg < ENS_TSIT5 || alg > ENS_EM || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (alg < ENS_TSIT5 || alg > ENS_SIEA || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
   const bool sde = nw > 0;
-  if (sde != (alg == ENS_EM)) return ENS_E_ALG_MISMATCH;
+  if (sde != is_sde_alg(alg)) return ENS_E_ALG_MISMATCH;
   // events (DESIGN R18) are located on the adaptive Tsit5 interpolant only
   if (model == ENS_BALL && (alg != ENS_TSIT5 || !opt->adaptive)) return ENS_E_UNSUPPORTED;
-  if (alg == ENS_EM && opt->adaptive) return ENS_E_ADAPTIVE_UNSUPPORTED;
+  if (is_sde_alg(alg) && opt->adaptive) return ENS_E_ADAPTIVE_UNSUPPORTED;
   if (!std::isfinite(t0) || !std::isfinite(tf) || !std::isfinite(dt) || !(t0 < tf) || !(dt > 0))
     return ENS_E_BAD_TSPAN;
   if (opt->adaptive) {
@@ -299,7 +309,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
       for (int j = 0; j < a.k; ++j) tau[j] = (T)opt->saveat[j];
       if (cudaMemcpyAsync(ws + L.tau, tau.data(), sizeof(T) * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return ENS_E_CUDA;
-      if (alg == ENS_EM) {
+      if (is_sde_alg(alg)) {
         std::vector<int64_t> st;
         if (!em_save_steps(t0, tf, dt, opt->saveat, a.k, st)) return ENS_E_BAD_SAVEAT;
         if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -313,11 +323,11 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   ens_status st = dispatch<T>(model, alg, a, opt, s);
   if (st != ENS_OK) return st;
   if (opt->want_stats) {
-    if (alg != ENS_EM) {
+    if (!is_sde_alg(alg)) {
       const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
       stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, kStatsChunk, a.partial);
     }
-    const int64_t nparts = (alg == ENS_EM) ? (int64_t)grid_for<T>(N).x : L.nparts;
+    const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for<T>(N).x : L.nparts;
     stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
     if (cudaPeekAtLastError() != cudaSuccess) return ENS_E_CUDA;
   }
@@ -350,9 +360,9 @@ ens_status ensemble_solve(ens_model model, ens_alg alg, ens_dtype dtype, int64_t
   ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
   if (st != ENS_OK) return st;
   if (!out || !u0 || !p) return ENS_E_INVALID_ARG;
-  if (!out->u_out && !(alg == ENS_EM && opt->want_stats)) return ENS_E_INVALID_ARG;
+  if (!out->u_out && !(is_sde_alg(alg) && opt->want_stats)) return ENS_E_INVALID_ARG;
   if (opt->want_stats && !out->stats) return ENS_E_INVALID_ARG;
-  if (alg == ENS_EM && opt->n_saveat > 0) {
+  if (is_sde_alg(alg) && opt->n_saveat > 0) {
     std::vector<int64_t> tmp;
     if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
   }
@@ -370,7 +380,7 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   int n = 0, m = 0, nw = 0;
   ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
   if (st != ENS_OK) return st;
-  if (alg == ENS_EM || opt->want_stats) return ENS_E_UNSUPPORTED;
+  if (is_sde_alg(alg) || opt->want_stats) return ENS_E_UNSUPPORTED;
   if (!u0_host || !p_host || !d_u0 || !d_p || !d_u_out || !u_out_host) return ENS_E_INVALID_ARG;
   if (!workspace || workspace_bytes < ens_workspace_bytes(model, alg, dtype, N, opt)) return ENS_E_WORKSPACE;
   model_dims(model, &n, &m, &nw);
