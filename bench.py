@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--no-gather", action="store_true", help="skip the NCCL gather of final states (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-also", action="store_true", help="skip the fp64-fixed / adaptive side measurements")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N>1 (gloo: test the multi-rank path on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -184,10 +186,16 @@ def main():
     import paper_2304_06835_b200 as ens
     from paper_2304_06835_b200 import multi_gpu as mg
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one rank per GPU (the driver's launch); --backend gloo lets several ranks share a GPU
+    # to exercise the multi-rank path where only one GPU exists (never for reported numbers)
+    gpu = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     N = args.n
     shard = mg.shard_weak(N, rank, world)
@@ -235,7 +243,7 @@ def main():
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         ev0.record(stream)
         for s in range(args.steps):
             step(*kev[s])

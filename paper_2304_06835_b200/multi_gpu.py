@@ -58,12 +58,19 @@ def shard_weak(n_per_rank: int, rank: int, world: int) -> Shard:
     return Shard(rank, world, n_per_rank, rank * n_per_rank)
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo moves CUDA tensors through host memory (used only to exercise the
+    multi-rank path on a single GPU; NCCL works on device tensors directly)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def allgather_stats(local: torch.Tensor, group=None) -> torch.Tensor:
     """[k, n, 3] per-rank (count, mean, M2) → [R, k, n, 3] on every rank."""
     R = dist.get_world_size(group)
-    out = torch.empty((R * local.shape[0], *local.shape[1:]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
-    return out.view(R, *local.shape)
+    src = local.cpu() if _host_staged(local, group) else local.contiguous()
+    out = torch.empty((R * src.shape[0], *src.shape[1:]), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out.view(R, *local.shape).to(local.device)
 
 
 def merge_stats(gathered: torch.Tensor) -> torch.Tensor:
@@ -79,9 +86,10 @@ def gather_states(local: torch.Tensor, dst: int = 0, group=None) -> Optional[tor
     Returns [R, ..., N_r] on dst, None elsewhere."""
     R = dist.get_world_size(group)
     me = dist.get_rank(group)
+    src = local.cpu() if _host_staged(local, group) else local.contiguous()
     if me == dst:
-        bufs = [torch.empty_like(local) for _ in range(R)]
-        dist.gather(local.contiguous(), gather_list=bufs, dst=dst, group=group)
-        return torch.stack(bufs)
-    dist.gather(local.contiguous(), dst=dst, group=group)
+        bufs = [torch.empty_like(src) for _ in range(R)]
+        dist.gather(src, gather_list=bufs, dst=dst, group=group)
+        return torch.stack(bufs).to(local.device)
+    dist.gather(src, dst=dst, group=group)
     return None
