@@ -135,7 +135,7 @@ def run_reference(args, rank):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    N = args.n
+    N = args.traj_per_gpu
     vals = []
     sample = args.ref_sample
     for _ in range(args.warmup):
@@ -159,7 +159,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=10**7, help="trajectories per GPU")
+    ap.add_argument("--traj-per-gpu", type=int, default=10**7, help="trajectories per GPU (N)")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=98304)
@@ -197,7 +197,7 @@ def main():
         else:
             dist.init_process_group("gloo")
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
-    N = args.n
+    N = args.traj_per_gpu
     shard = mg.shard_weak(N, rank, world)
     N_total = N * world
     tspan, dt = (0.0, 1.0), 1e-3

@@ -12,6 +12,11 @@ if str(ROOT) not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) device; run with -m gpu")
     config.addinivalue_line("markers", "slow: longer CPU test")
+    # the sm_100a library cross-compiles without a GPU; build it once if this checkout lacks it
+    lib = ROOT / "paper_2304_06835_b200" / "libens.so"
+    if not lib.exists():
+        from paper_2304_06835_b200 import _build
+        _build.build()
 
 
 def pytest_collection_modifyitems(config, items):
