@@ -102,8 +102,9 @@ typedef struct {
                               time must lie on the step grid (DESIGN R11). */
   int32_t n_saveat;        /* k >= 0; 0 -> only the final state is stored */
   int32_t p_broadcast;     /* 1: p is [m], shared by all trajectories */
-  int32_t want_stats;      /* 1: ensemble (count, mean, M2) per save point & component;
-                              over trajectories with retcode SUCCESS (DESIGN R12) */
+  int32_t want_stats;      /* 1: ensemble (count, mean, M2) per save point & component,
+                              over the finite values (failed / unreached entries are NaN and
+                              excluded; DESIGN R12). Deterministic for a fixed N and launch. */
   int32_t refill;          /* adaptive only: 1 = warp-ballot lane retire/refill scheduler (a8) */
   int64_t index_offset;    /* global index of local trajectory 0 (Philox counter; multi-GPU shard) */
   int64_t chunk_len, chunk_stride; /* 0,0: contiguous. Else global(i) = index_offset +
@@ -114,7 +115,7 @@ typedef struct {
   void* u_out;             /* device T: [k][n][N] if k > 0 else [n][N]. Required except EM with
                               want_stats (may be NULL: statistics only). Unreached save points of a
                               failed trajectory are NaN (DESIGN R6). */
-  int32_t* retcode;        /* device [N] or NULL (required when want_stats with an ODE algorithm) */
+  int32_t* retcode;        /* device [N] or NULL */
   int32_t* n_accept;       /* device [N] or NULL */
   int32_t* n_reject;       /* device [N] or NULL */
   double* stats;           /* device [max(k,1)][n][3] = (count, mean, M2) fp64, or NULL */

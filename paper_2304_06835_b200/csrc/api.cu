@@ -91,11 +91,6 @@ int sm_count() {
   return cached;
 }
 
-template <class K>
-ens_status launch_check() {
-  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
-}
-
 // Block size of a one-thread-per-trajectory launch: 256 once the ensemble
 // fills every SM with 256-thread blocks, otherwise smaller (down to one warp)
 // so that small ensembles — C1's 1024 trajectories, the stiff suite's 8192 —
