@@ -144,8 +144,10 @@ ens_status ensemble_solve(ens_model model, ens_alg alg, ens_dtype dtype, int64_t
  * streams (stream + one the call creates and destroys). Device buffers:
  * d_u0 [n][N], d_p [m][N] (or [m]), d_u_out like u_out, d_retcode [N];
  * out->u_out/retcode are ignored (the staging buffers are used). Synchronous:
- * returns after the last copy completed. EM/stats not supported here
- * (ENS_E_UNSUPPORTED). */
+ * returns after the last copy completed. SDE solvers (EM/SIEA) key each
+ * chunk's Philox counters on its global indices (index_offset + chunk start),
+ * so results equal one ensemble_solve call; a block-cyclic map
+ * (chunk_len > 0) with n_chunks > 1 and want_stats are ENS_E_UNSUPPORTED. */
 ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, int64_t N,
                                const void* u0_host, const void* p_host, double t0, double tf, double dt,
                                const ens_options* opt, void* d_u0, void* d_p, void* d_u_out,

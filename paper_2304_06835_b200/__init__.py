@@ -203,7 +203,7 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
 
 def solve_host(model: str, alg: str, u0_host: torch.Tensor, p_host: torch.Tensor, tspan, dt, *, device=None,
                adaptive=False, abstol=1e-6, reltol=1e-3, saveat=None, max_steps=0, refill=False, n_chunks=4,
-               staging=None, u_out_host=None, retcode_host=None, stream=None):
+               seed=0, index_offset=0, staging=None, u_out_host=None, retcode_host=None, stream=None):
     """ensemble_solve_host: host (pinned) inputs → chunked H2D / solve / D2H overlapped → host outputs."""
     import numpy as np
     dev = torch.device(device or "cuda")
@@ -211,7 +211,7 @@ def solve_host(model: str, alg: str, u0_host: torch.Tensor, p_host: torch.Tensor
     p_broadcast = p_host.dim() == 1
     sa = None if saveat is None else np.ascontiguousarray(np.asarray(saveat, dtype=np.float64))
     k = 0 if sa is None else sa.size
-    opt = _options(adaptive, abstol, reltol, max_steps, 0, sa, p_broadcast, False, refill, 0, 0, 0)
+    opt = _options(adaptive, abstol, reltol, max_steps, seed, sa, p_broadcast, False, refill, index_offset, 0, 0)
     L = lib()
     dt_ = u0_host.dtype
     wsb = L.ens_workspace_bytes(MODELS[model], ALGS[alg], DTYPES[dt_], N, ctypes.byref(opt))

@@ -375,13 +375,22 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   int n = 0, m = 0, nw = 0;
   ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
   if (st != ENS_OK) return st;
-  if (is_sde_alg(alg) || opt->want_stats) return ENS_E_UNSUPPORTED;
+  if (opt->want_stats) return ENS_E_UNSUPPORTED;
   if (!u0_host || !p_host || !d_u0 || !d_p || !d_u_out || !u_out_host) return ENS_E_INVALID_ARG;
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(n_chunks, N));
+  if (is_sde_alg(alg)) {
+    // Philox counters key on the global trajectory index (DESIGN R10): each chunk
+    // shifts index_offset by its start; a block-cyclic map cannot be split that way.
+    if (opt->chunk_len > 0 && C > 1) return ENS_E_UNSUPPORTED;
+    if (opt->n_saveat > 0) {
+      std::vector<int64_t> tmp;
+      if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
+    }
+  }
   if (!workspace || workspace_bytes < ens_workspace_bytes(model, alg, dtype, N, opt)) return ENS_E_WORKSPACE;
   model_dims(model, &n, &m, &nw);
   const size_t ts = dtype == ENS_F32 ? 4 : 8;
   const int kk = std::max(1, opt->n_saveat);
-  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(n_chunks, N));
   cudaStream_t s = (cudaStream_t)stream;
   cudaStream_t sh = nullptr, sd = nullptr;
   if (cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking) != cudaSuccess) return ENS_E_CUDA;
@@ -417,6 +426,7 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
     out.u_out = (char*)d_u_out + lo * ts;
     out.retcode = d_retcode ? d_retcode + lo : nullptr;
     ens_options o = *opt;
+    if (o.chunk_len == 0) o.index_offset = opt->index_offset + lo;
     const void* pp = opt->p_broadcast ? d_p : (const void*)((const char*)d_p + lo * ts);
     if (dtype == ENS_F32)
       st = solve_impl<float>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, s, c == 0);
