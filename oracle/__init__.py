@@ -24,7 +24,7 @@ _LIB = _HERE / "liboracle.so"
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
           "expdecay": 5, "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10,
           "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
         L.orc_diffusion.argtypes = [i32, i32, vp, vp, dbl, vp]
         L.orc_tsit5_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_ros23_consts.argtypes = [vp, vp]
+        L.orc_rodas4_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_controller.argtypes = [i32, vp]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_pi.argtypes = [i32, i32, dbl, dbl, ctypes.POINTER(dbl)]
@@ -122,6 +123,13 @@ def ros23_consts():
     d = np.zeros(1); e = np.zeros(1)
     lib().orc_ros23_consts(_p(d), _p(e))
     return float(d[0]), float(e[0])
+
+
+def rodas4_tableau():
+    """(gamma, A[6,6], C[6,6], D[2,5]) of the Rodas4 W-form (DESIGN R20)."""
+    g = np.zeros(1); A = np.zeros((6, 6)); C = np.zeros((6, 6)); D = np.zeros((2, 5))
+    lib().orc_rodas4_tableau(_p(g), _p(A), _p(C), _p(D))
+    return float(g[0]), A, C, D
 
 
 def controller(alg: str):

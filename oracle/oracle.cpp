@@ -40,7 +40,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -891,6 +891,163 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
   }
 }
 
+// ---------------------------------------------------------------- Rodas4 ----
+// GPURodas4 (NEXT-2). The paper names the method but prints no
+// coefficients; DESIGN R20: the RODAS tableau of Hairer & Wanner (Solving ODEs
+// II, §IV.7) in their W-form
+//   (1/(hγ) I − J) k_i = f(u + Σ_{j<i} a_ij k_j) + Σ_{j<i} (c_ij/h) k_j,
+// stiffly accurate: stage 6 is evaluated at Y6 = Y5 + k5, u_new = Y6 + k6 and
+// the embedded (order-3) solution is Y6, so the error estimate is E = k6.
+// Pinned by the Rosenbrock order conditions (tests/test_oracle_rodas4.py).
+static const double RD_GAMMA = 0.25;
+static const double RD_A[6][5] = {
+  {0, 0, 0, 0, 0},
+  {1.544, 0, 0, 0, 0},
+  {0.9466785280815826, 0.2557011698983284, 0, 0, 0},
+  {3.314825187068521, 2.896124015972201, 0.9986419139977817, 0, 0},
+  {1.221224509226641, 6.019134481288629, 12.53708332932087, -0.6878860361058950, 0},
+  {1.221224509226641, 6.019134481288629, 12.53708332932087, -0.6878860361058950, 1.0}};
+static const double RD_C[6][5] = {
+  {0, 0, 0, 0, 0},
+  {-5.6688, 0, 0, 0, 0},
+  {-2.430093356833875, -0.2063599157091915, 0, 0, 0},
+  {-0.1073529058151375, -9.594562251023355, -20.47028614809616, 0, 0},
+  {7.496443313967647, -10.24680431464352, -33.99990352819905, 11.70890893206160, 0},
+  {8.083246795921522, -7.981132988064893, -31.52159432874371, 16.31930543123136, -6.058818238834054}};
+// continuous extension u(t+θh) = (1−θ)u + θ(u_new + (1−θ)(s1 + θ s2)),
+// s1 = Σ_{j≤5} D2_j k_j, s2 = Σ_{j≤5} D3_j k_j (Hairer & Wanner's RODAS dense output)
+static const double RD_D2[5] = {10.12623508344586, -7.487995877610167, -34.80091861555747, -7.992771707568823,
+                                1.025137723295662};
+static const double RD_D3[5] = {-0.6762803392801253, 6.087714651680015, 16.43084320892478, 24.76722511418386,
+                                -6.594389125716872};
+static const Ctrl CTRL_RODAS4 = {7.0 / 40.0, 2.0 / 20.0, 0.9, 5.0, 0.1, 1e-4};   // p=4
+
+// One Rodas4 step (autonomous models: ∂f/∂t = 0, so the d_i h f_t terms vanish).
+// F0 = f(u). Outputs u_new, K[0..5] = k1..k6, E = k6. false if W is singular.
+template <class T>
+static bool rodas4_step(int model, int n, const T* p, T t, T h, const T* u, const T* F0, T* unew, T (*K)[NMAX],
+                        T* E) {
+  T J[NMAX * NMAX], W[NMAX * NMAX], inv[NMAX]; int piv[NMAX];
+  jac<T>(model, u, p, t, J);
+  const T hg = h * (T)RD_GAMMA;
+  const T ihg = T(1) / hg;                                             // 1/(hγ)
+  const T ih = T(1) / h;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) W[i * n + j] = (i == j ? ihg : T(0)) - J[i * n + j];   // W = I/(hγ) − J
+  if (!lu_factor<T>(n, W, piv, inv)) return false;
+  lu_solve<T>(n, W, piv, inv, F0, K[0]);                               // k1 = W⁻¹ f(u)
+  T y[NMAX], F[NMAX], r[NMAX];
+  for (int s = 1; s < 6; ++s) {
+    // stage argument Y_s = u + Σ_{j<s} a_sj k_j (for s = 6: Y5 + k5, a_65 = 1)
+    for (int c = 0; c < n; ++c) {
+      T acc = u[c];
+      for (int j = 0; j < s; ++j) acc = std::fma((T)RD_A[s][j], K[j][c], acc);
+      y[c] = acc;
+    }
+    rhs<T>(model, y, p, t, F);
+    // r = f(Y_s) + Σ_{j<s} (c_sj/h) k_j
+    for (int c = 0; c < n; ++c) {
+      T acc = F[c];
+      for (int j = 0; j < s; ++j) acc = std::fma((T)RD_C[s][j] * ih, K[j][c], acc);
+      r[c] = acc;
+    }
+    lu_solve<T>(n, W, piv, inv, r, K[s]);
+  }
+  for (int c = 0; c < n; ++c) { unew[c] = y[c] + K[5][c]; E[c] = K[5][c]; }   // u_new = Y6 + k6
+  return true;
+}
+
+template <class T>
+static void rodas4_interp(int n, T theta, const T* u, const T* unew, const T (*K)[NMAX], T* out) {
+  const T th1 = T(1) - theta;
+  for (int c = 0; c < n; ++c) {
+    T s1 = (T)RD_D2[0] * K[0][c], s2 = (T)RD_D3[0] * K[0][c];
+    for (int j = 1; j < 5; ++j) { s1 = std::fma((T)RD_D2[j], K[j][c], s1); s2 = std::fma((T)RD_D3[j], K[j][c], s2); }
+    const T inner = std::fma(theta, s2, s1);                            // s1 + θ s2
+    const T w = std::fma(th1, inner, unew[c]);                          // u_new + (1−θ)(…)
+    out[c] = std::fma(th1, u[c], theta * w);                            // (1−θ)u + θ w
+  }
+}
+
+template <class T>
+static void solve_rodas4(const Opts& o, Traj<T>& tr) {
+  const int n = tr.n, model = o.model;
+  const Ctrl& C = CTRL_RODAS4;
+  T u[NMAX], F0[NMAX], unew[NMAX], K[6][NMAX], E[NMAX];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  const int k = o.k;
+  std::vector<T> tau(k);
+  for (int j = 0; j < k; ++j) tau[j] = (T)o.saveat[j];
+  int js = 0;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  T t = (T)o.t0;
+  const T tf = (T)o.tf, abstol = (T)o.abstol, reltol = (T)o.reltol;
+  rhs<T>(model, u, p, t, F0);
+  while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; }
+  auto save_in_step = [&](T t0s, T tn, T h) {
+    while (js < k && tau[js] <= tn) {
+      if (tau[js] == tn) put(tr.save, n, js, unew);
+      else { T out[NMAX]; rodas4_interp<T>(n, (tau[js] - t0s) / h, u, unew, K, out); put(tr.save, n, js, out); }
+      ++js;
+    }
+  };
+  if (!finite_vec(F0, n)) tr.retcode = RET_DIVERGED;
+  else if (!o.adaptive) {
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    const T hdt = (T)o.dt, hl = (T)h_last;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const bool last = (i == nsteps - 1);
+      const T h = last ? hl : hdt;
+      t = (T)(o.t0 + (double)i * o.dt);
+      if (!rodas4_step<T>(model, n, p, t, h, u, F0, unew, K, E)) { tr.retcode = RET_SINGULAR; break; }
+      save_in_step(t, last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt), h);
+      for (int j = 0; j < n; ++j) u[j] = unew[j];
+      rhs<T>(model, u, p, last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt), F0);
+      tr.n_accept++;
+    }
+    t = tf;
+    if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  } else {
+    T h = (T)std::min(o.dt, o.tf - o.t0);
+    T lq_old = (T)L_FLOOR;
+    int64_t attempts = 0;
+    while (t < tf) {
+      if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
+      const bool last = (t + h >= tf);
+      if (last) h = tf - t;
+      ++attempts;
+      if (!rodas4_step<T>(model, n, p, t, h, u, F0, unew, K, E)) {
+        h = h * T(0.5);                                   // singular W: reject, halve (DESIGN R10)
+        tr.n_reject++;
+        if (t + h == t) { tr.retcode = RET_SINGULAR; break; }
+        continue;
+      }
+      const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
+      if (q2 < T(1)) {
+        const T tn = last ? tf : t + h;
+        save_in_step(t, tn, h);
+        t = tn;
+        for (int j = 0; j < n; ++j) u[j] = unew[j];
+        rhs<T>(model, u, p, t, F0);
+        tr.n_accept++;
+        h = pi_accept<T>(C, h, q2, &lq_old);
+      } else {
+        h = pi_reject<T>(C, h, q2);
+        tr.n_reject++;
+      }
+      if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
+    }
+  }
+  if (k == 0) put(tr.save, n, 0, u);
+  else {
+    const T nan = std::numeric_limits<T>::quiet_NaN();
+    T nv[NMAX]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    for (; js < k; ++js) put(tr.save, n, js, nv);
+  }
+}
+
 // --------------------------------------------------------- Euler–Maruyama ----
 // u_{i+1} = u_i + h a(u_i,t_i) + b(u_i,t_i) ⊙ ΔW_i, ΔW_i = √h Z_i ~ N(0, h I)
 // (P:153-157). Fixed grid (DESIGN R3); saveat on grid points (DESIGN R11).
@@ -1011,6 +1168,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     tr.save = buf.data();
     if (o.alg == TSIT5) solve_tsit5<T>(o, tr);
     else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
+    else if (o.alg == RODAS4) solve_rodas4<T>(o, tr);
     else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
     for (int s = 0; s < kk; ++s)
@@ -1060,15 +1218,28 @@ void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
   }
 }
 void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
+static const orc::Ctrl& ctrl_of(int alg) {
+  return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4 : orc::CTRL_TSIT5;
+}
+// Rodas4 tableau export for the order-condition pins: gamma, A[36], C[36] (6×6 row-major, strictly lower), D[10].
+void orc_rodas4_tableau(double* gamma, double* A, double* C, double* D) {
+  *gamma = orc::RD_GAMMA;
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) {
+      A[i * 6 + j] = j < 5 ? orc::RD_A[i][j] : 0.0;
+      C[i * 6 + j] = j < 5 ? orc::RD_C[i][j] : 0.0;
+    }
+  for (int j = 0; j < 5; ++j) { D[j] = orc::RD_D2[j]; D[5 + j] = orc::RD_D3[j]; }
+}
 void orc_controller(int alg, double* out6) {
-  const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
+  const orc::Ctrl& C = ctrl_of(alg);
   out6[0] = C.beta1; out6[1] = C.beta2; out6[2] = C.eta; out6[3] = C.qmin_inv; out6[4] = C.qmax_inv;
   out6[5] = C.qold_floor;
 }
 
 // Controller / error-norm pins (fp64): returns h_new; *lq_old (= log2 q_old) updated on accept.
 double orc_pi(int alg, int accept, double h, double q2, double* lq_old) {
-  const orc::Ctrl& C = (alg == orc::ROSENBROCK23) ? orc::CTRL_ROS23 : orc::CTRL_TSIT5;
+  const orc::Ctrl& C = ctrl_of(alg);
   return accept ? orc::pi_accept<double>(C, h, q2, lq_old) : orc::pi_reject<double>(C, h, q2);
 }
 double orc_log2(int dtype, double x) {
