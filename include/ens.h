@@ -54,7 +54,7 @@ typedef enum {
   ENS_RET_MAXITERS = 1,   /* attempted steps reached max_steps */
   ENS_RET_DTMIN = 2,      /* t + h == t in T (step size underflow) */
   ENS_RET_DIVERGED = 3,   /* f(u0) non-finite, or (fixed step) final state non-finite (DESIGN R6) */
-  ENS_RET_SINGULAR = 4    /* Rosenbrock W = I − h d J singular and h can no longer shrink (DESIGN R10) */
+  ENS_RET_SINGULAR = 4    /* Rosenbrock W (I − h d J or I/(hγ) − J) singular and h can no longer shrink (R10) */
 } ens_retcode;
 
 typedef enum {
@@ -68,7 +68,7 @@ typedef enum {
   ENS_CRN = 7,             /* n=4, m=6 p=(S,D,τ,ν0,n,η), 8 Wiener: σ-factor CRN SDE, P:690-725 (DESIGN R14) */
   ENS_OREGO = 8,           /* n=3,  m=3  stiff Oregonator, P:739-749 (AD Jacobian, DESIGN R15) */
   ENS_HIRES = 9,           /* n=8,  m=12 stiff HIRES, P:751-776 (AD Jacobian) */
-  ENS_POLLU = 10,          /* n=20, m=25 stiff POLLU, P:779-833 (AD Jacobian; Rosenbrock23 only) */
+  ENS_POLLU = 10,          /* n=20, m=25 stiff POLLU, P:779-833 (AD Jacobian; Rosenbrock23 / Rodas4, fp64 only) */
   ENS_BALL = 11            /* n=2, m=2 p=(g,e) bouncing ball with an event (x crosses 0 ↓ → v ← −e v),
                               P:514-524; adaptive Tsit5 only (DESIGN R18) */
 } ens_model;
@@ -77,7 +77,9 @@ typedef enum {
   ENS_TSIT5 = 0,           /* Tsitouras 5(4), FSAL, free 4th-order interpolant */
   ENS_ROSENBROCK23 = 1,    /* ode23s Rosenbrock-W 2(3), ode23s interpolant */
   ENS_EM = 2,              /* Euler–Maruyama, fixed step, diagonal or model-defined noise */
-  ENS_SIEA = 3             /* weak order 2.0 stochastic improved Euler, fixed step, diagonal noise (R19) */
+  ENS_SIEA = 3,            /* weak order 2.0 stochastic improved Euler, fixed step, diagonal noise (R19) */
+  ENS_RODAS4 = 4           /* 4th-order stiffly accurate Rosenbrock, L-stable, fixed or adaptive (R20);
+                              ODE models without events; POLLU fp64 only */
 } ens_alg;
 
 typedef enum { ENS_F32 = 0, ENS_F64 = 1 } ens_dtype;

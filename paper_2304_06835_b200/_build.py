@@ -1,20 +1,28 @@
 """Build the sm_100a shared library libens.so in-tree (nvcc cross-compiles
 without a GPU). Flags: --fmad=false (only the explicit fmas of DESIGN §4 are
-fused), no fast-math (IEEE div/sqrt, no FTZ), -lineinfo for ncu source views."""
+fused), no fast-math (IEEE div/sqrt, no FTZ), -lineinfo for ncu source views.
+
+One translation unit per algorithm (csrc/k_*.cu) plus the ABI (csrc/api.cu),
+compiled in parallel into csrc/../_obj/*.o (each rebuilt only when a file it
+includes changed, from nvcc's -MD dependency lists), then linked."""
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB = PKG / "libens.so"
-SRCS = sorted((PKG / "csrc").glob("*.cu")) + sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "ens.h"]
+OBJ = PKG / "_obj"
+CSRC = PKG / "csrc"
+UNITS = sorted(CSRC.glob("*.cu"))
+SRCS = UNITS + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ens.h"]
 
-NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
-              "-Xcompiler", "-fPIC", "-shared"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC"]
 
 
 def nvcc() -> str:
@@ -24,16 +32,45 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    newest = max(s.stat().st_mtime for s in SRCS)
-    if not force and LIB.exists() and LIB.stat().st_mtime >= newest:
-        return LIB
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), str(PKG / "csrc" / "api.cu")]
+def _deps(unit: Path) -> list[Path]:
+    d = OBJ / (unit.stem + ".d")
+    if not d.exists():
+        return SRCS
+    text = d.read_text().replace("\\\n", " ")
+    paths = text.split(":", 1)[1].split() if ":" in text else []
+    return [Path(p) for p in paths] or SRCS
+
+
+def _stale(unit: Path) -> bool:
+    o = OBJ / (unit.stem + ".o")
+    if not o.exists():
+        return True
+    t = o.stat().st_mtime
+    return any((not p.exists()) or p.stat().st_mtime > t for p in _deps(unit))
+
+
+def _compile(unit: Path, verbose: bool) -> None:
+    o = OBJ / (unit.stem + ".o")
+    tmp = o.with_suffix(f".o.tmp{os.getpid()}")
+    cmd = [nvcc(), *NVCC_FLAGS, "-MD", "-MF", str(OBJ / (unit.stem + ".d")), "-c", "-o", str(tmp), str(unit)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    os.replace(tmp, o)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    OBJ.mkdir(exist_ok=True)
+    todo = [u for u in UNITS if force or _stale(u)]
+    objs = [OBJ / (u.stem + ".o") for u in UNITS]
+    if not todo and LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return LIB
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_compile, u, verbose) for u in todo]:
+            f.result()
+    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
     os.replace(tmp, LIB)
     return LIB
 

@@ -13,18 +13,24 @@
 #include "common.cuh"
 #include "em.cuh"
 #include "inputs.cuh"
-#include "models.cuh"
-#include "models_stiff.cuh"
-#include "ros23.cuh"
-#include "sched.cuh"
+#include "launch.cuh"
 #include "stats.cuh"
-#include "tsit5.cuh"
 
 using namespace ens;
 
+int ens::sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
 namespace {
 
-constexpr int kBlock = 256;
 constexpr int64_t kStatsChunk = 8192;
 
 bool model_dims(int model, int* n, int* m, int* nw) {
@@ -45,7 +51,6 @@ bool model_dims(int model, int* n, int* m, int* nw) {
 
 inline bool is_sde_alg(int alg) { return alg == ENS_EM || alg == ENS_SIEA; }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // DESIGN R3: fixed-step count and last step, in fp64.
 void fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last) {
@@ -80,144 +85,15 @@ Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
   return L;
 }
 
-int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
-}
-
-// Block size of a one-thread-per-trajectory launch: 256 once the ensemble
-// fills every SM with 256-thread blocks, otherwise smaller (down to one warp)
-// so that small ensembles — C1's 1024 trajectories, the stiff suite's 8192 —
-// spread over all SMs instead of a handful (the latency-bound regime).
-int solver_block(int64_t threads) {
-  const int64_t per_sm = cdiv(threads, sm_count());
-  return (int)std::min<int64_t>(kBlock, std::max<int64_t>(32, cdiv(per_sm, 32) * 32));
-}
-template <class T>
-dim3 grid_for(int64_t N) { return dim3((unsigned)cdiv(N, solver_block(N))); }
-
 // ---------------------------------------------------------------- dispatch --
-template <class M, class T>
-ens_status run_ode(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
-  const bool save = a.k > 0;
-  const dim3 g = grid_for<T>(a.N), b(solver_block(a.N));
-  if constexpr (M::n > 8) {
-    // POLLU (n = 20) is built for its stiff solver only (register-resident Tsit5 stages for
-    // n = 20 are not instantiated)
-    if (alg == ENS_TSIT5) return ENS_E_UNSUPPORTED;
-  }
-  if (alg == ENS_TSIT5) {
-   if constexpr (M::n <= 8) {
-    if (!opt->adaptive) {
-      if constexpr (std::is_same<T, float>::value) {
-        // fp32: two trajectories per thread on the packed FFMA2 path
-        const auto cf = make_tsit_coef<float, float2>(a.dt0, a.h_last);
-        const int64_t threads = cdiv(a.N, 2);
-        const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
-        if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b2, 0, s>>>(a, cf);
-        else tsit5_fixed_kernel<M, f2, false><<<g2, b2, 0, s>>>(a, cf);
-      } else {
-        const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
-        if (save) tsit5_fixed_kernel<M, double, true><<<g, b, 0, s>>>(a, cf);
-        else tsit5_fixed_kernel<M, double, false><<<g, b, 0, s>>>(a, cf);
-      }
-    } else if (opt->refill) {
-      int occ = 0;
-      if (save) {
-        auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, true>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
-        kern<<<gr, b, 0, s>>>(a);
-      } else {
-        auto kern = adaptive_refill_kernel<Tsit5Lane<M, T, false>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
-        kern<<<gr, b, 0, s>>>(a);
-      }
-    } else {
-      // (a two-trajectories-per-thread f2 variant of the adaptive step measured 4 % slower:
-      //  90 vs 48 registers halves residency, per-lane control flow stays scalar —
-      //  profiles/pair_adaptive_r01.log; the fixed-step kernel is where packing pays)
-      if (save) adaptive_static_kernel<Tsit5Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
-      else adaptive_static_kernel<Tsit5Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
-    }
-   }
-  } else {  // Rosenbrock23
-    if (!opt->adaptive) {
-      if (save) ros23_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
-      else ros23_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
-    } else if (opt->refill) {
-      int occ = 0;
-      if (save) {
-        auto kern = adaptive_refill_kernel<Ros23Lane<M, T, true>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
-        kern<<<gr, b, 0, s>>>(a);
-      } else {
-        auto kern = adaptive_refill_kernel<Ros23Lane<M, T, false>, T>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
-        const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
-        kern<<<gr, b, 0, s>>>(a);
-      }
-    } else {
-      // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
-      // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log). ENS_TUNE_ROS23_MINB=1 reverts.
-      static const int minb = [] {
-        const char* e = getenv("ENS_TUNE_ROS23_MINB");
-        return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
-      }();
-      if (minb == 3) {
-        if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T, 3><<<g, b, 0, s>>>(a);
-        else adaptive_static_kernel<Ros23Lane<M, T, false>, T, 3><<<g, b, 0, s>>>(a);
-      } else {
-        if (save) adaptive_static_kernel<Ros23Lane<M, T, true>, T><<<g, b, 0, s>>>(a);
-        else adaptive_static_kernel<Ros23Lane<M, T, false>, T><<<g, b, 0, s>>>(a);
-      }
-    }
-  }
-  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
-}
-
-template <class M, class T>
-ens_status run_sde(int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
-  const dim3 g = grid_for<T>(a.N), b(solver_block(a.N));
-  if (alg == ENS_SIEA) {
-    if constexpr (M::nw == M::n) {   // diagonal noise only
-      if (opt->want_stats) em_kernel<M, T, true, true><<<g, b, 0, s>>>(a);
-      else em_kernel<M, T, false, true><<<g, b, 0, s>>>(a);
-    } else {
-      return ENS_E_UNSUPPORTED;
-    }
-  } else {
-    if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
-    else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
-  }
-  return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
-}
-
+// Kernel instances live in one translation unit per algorithm (launch.cuh).
 template <class T>
 ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
-  switch (model) {
-    case ENS_LORENZ: return run_ode<Lorenz, T>(alg, a, opt, s);
-    case ENS_ROBERTSON: return run_ode<Robertson, T>(alg, a, opt, s);
-    case ENS_EXPDECAY: return run_ode<ExpDecay, T>(alg, a, opt, s);
-    case ENS_HARMONIC: return run_ode<Harmonic, T>(alg, a, opt, s);
-    case ENS_LORENZ_SDE_ADD: return run_sde<LorenzSDE<false>, T>(alg, a, opt, s);
-    case ENS_LORENZ_SDE_MUL: return run_sde<LorenzSDE<true>, T>(alg, a, opt, s);
-    case ENS_GBM: return run_sde<GBM, T>(alg, a, opt, s);
-    case ENS_CRN: return run_sde<CRN, T>(alg, a, opt, s);
-    case ENS_OREGO: return run_ode<Orego, T>(alg, a, opt, s);
-    case ENS_HIRES: return run_ode<Hires, T>(alg, a, opt, s);
-    case ENS_BALL: return run_ode<Ball, T>(alg, a, opt, s);
-    case ENS_POLLU:   // fp64 only (20 × 21 dual numbers per AD Jacobian: the fp32 build is not worth its size)
-      if constexpr (sizeof(T) == 8) return run_ode<Pollu, T>(alg, a, opt, s);
-      else return ENS_E_UNSUPPORTED;
+  switch (alg) {
+    case ENS_TSIT5: return launch_tsit5<T>(model, a, opt, s);
+    case ENS_ROSENBROCK23: return launch_ros23<T>(model, a, opt, s);
+    case ENS_RODAS4: return launch_rodas4<T>(model, a, opt, s);
+    case ENS_EM: case ENS_SIEA: return launch_sde<T>(model, alg, a, opt, s);
   }
   return ENS_E_INVALID_ARG;
 }
@@ -227,13 +103,14 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
                     const ens_options* opt, int* n_out) {
   int n, m, nw;
   if (!opt || N < 1 || !model_dims(model, &n, &m, &nw)) return ENS_E_INVALID_ARG;
-  if (alg < ENS_TSIT5 || alg > ENS_SIEA || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (alg < ENS_TSIT5 || alg > ENS_RODAS4 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
   const bool sde = nw > 0;
   if (sde != is_sde_alg(alg)) return ENS_E_ALG_MISMATCH;
   // events (DESIGN R18) are located on the adaptive Tsit5 interpolant only
   if (model == ENS_BALL && (alg != ENS_TSIT5 || !opt->adaptive)) return ENS_E_UNSUPPORTED;
+  if (dtype == ENS_F32 && model == ENS_POLLU) return ENS_E_UNSUPPORTED;   // n = 20: fp64 stiff solvers only
   if (is_sde_alg(alg) && opt->adaptive) return ENS_E_ADAPTIVE_UNSUPPORTED;
   if (!std::isfinite(t0) || !std::isfinite(tf) || !std::isfinite(dt) || !(t0 < tf) || !(dt > 0))
     return ENS_E_BAD_TSPAN;
@@ -322,7 +199,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
       const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
       stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, kStatsChunk, a.partial);
     }
-    const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for<T>(N).x : L.nparts;
+    const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for(N).x : L.nparts;
     stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
     if (cudaPeekAtLastError() != cudaSuccess) return ENS_E_CUDA;
   }

@@ -1,0 +1,48 @@
+// k_ros23.cu — Rosenbrock23 kernel instances (fixed step; adaptive static or
+// refill) for the ODE models without events.
+#include <cstdlib>
+
+#include "launch.cuh"
+#include "ros23.cuh"
+
+namespace ens {
+
+template <class M, class T>
+ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  const bool save = a.k > 0;
+  if (!opt->adaptive) {
+    const dim3 g = grid_for(a.N), b(solver_block(a.N));
+    if (save) ros23_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
+    else ros23_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+  } else {
+    // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
+    // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log). ENS_TUNE_ROS23_MINB=1 reverts.
+    static const int minb = [] {
+      const char* e = getenv("ENS_TUNE_ROS23_MINB");
+      return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
+    }();
+    if (minb == 3 && !opt->refill) {
+      if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
+      else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
+    } else {
+      if (save) launch_adaptive<Ros23Lane<M, T, true>, T>(a, opt->refill, s);
+      else launch_adaptive<Ros23Lane<M, T, false>, T>(a, opt->refill, s);
+    }
+  }
+  return launch_status();
+}
+
+template <class T>
+ens_status launch_ros23(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  return with_ode_model(model, [&](auto mt) -> ens_status {
+    using M = decltype(mt);
+    if constexpr (HasEvent<M>::value) return ENS_E_UNSUPPORTED;                  // events: Tsit5 only (R18)
+    else if constexpr (M::n > 8 && sizeof(T) == 4) return ENS_E_UNSUPPORTED;     // POLLU: fp64 only
+    else return run_ros23<M, T>(a, opt, s);
+  });
+}
+
+template ens_status launch_ros23<float>(int, const Args<float>&, const ens_options*, cudaStream_t);
+template ens_status launch_ros23<double>(int, const Args<double>&, const ens_options*, cudaStream_t);
+
+}  // namespace ens

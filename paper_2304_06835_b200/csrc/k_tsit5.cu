@@ -1,0 +1,50 @@
+// k_tsit5.cu — Tsit5 kernel instances (fixed step: f2-packed fp32 / fp64;
+// adaptive: static or refill scheduling) for every ODE model with n ≤ 8.
+#include <type_traits>
+
+#include "launch.cuh"
+#include "tsit5.cuh"
+
+namespace ens {
+
+template <class M, class T>
+ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  const bool save = a.k > 0;
+  if (!opt->adaptive) {
+    if constexpr (std::is_same<T, float>::value) {
+      // fp32: two trajectories per thread on the packed FFMA2 path
+      const auto cf = make_tsit_coef<float, float2>(a.dt0, a.h_last);
+      const int64_t threads = cdiv(a.N, 2);
+      const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
+      if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b2, 0, s>>>(a, cf);
+      else tsit5_fixed_kernel<M, f2, false><<<g2, b2, 0, s>>>(a, cf);
+    } else {
+      const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
+      const dim3 g = grid_for(a.N), b(solver_block(a.N));
+      if (save) tsit5_fixed_kernel<M, double, true><<<g, b, 0, s>>>(a, cf);
+      else tsit5_fixed_kernel<M, double, false><<<g, b, 0, s>>>(a, cf);
+    }
+  } else {
+    // (a two-trajectories-per-thread f2 variant of the adaptive step measured 4 % slower:
+    //  90 vs 48 registers halves residency, per-lane control flow stays scalar —
+    //  profiles/pair_adaptive_r01.log; the fixed-step kernel is where packing pays)
+    if (save) launch_adaptive<Tsit5Lane<M, T, true>, T>(a, opt->refill, s);
+    else launch_adaptive<Tsit5Lane<M, T, false>, T>(a, opt->refill, s);
+  }
+  return launch_status();
+}
+
+template <class T>
+ens_status launch_tsit5(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  return with_ode_model(model, [&](auto mt) -> ens_status {
+    using M = decltype(mt);
+    // register-resident Tsit5 stages are instantiated for n ≤ 8 (POLLU, n = 20, is stiff-only)
+    if constexpr (M::n > 8) return ENS_E_UNSUPPORTED;
+    else return run_tsit5<M, T>(a, opt, s);
+  });
+}
+
+template ens_status launch_tsit5<float>(int, const Args<float>&, const ens_options*, cudaStream_t);
+template ens_status launch_tsit5<double>(int, const Args<double>&, const ens_options*, cudaStream_t);
+
+}  // namespace ens

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) stats_partial_kernel(const T* __restrict_
 
 // Merge partials [rows][nparts][3] → out [rows][3], one 256-thread block per
 // row: thread t folds parts t, t+256, … in order; then a fixed binary tree.
-__global__ void __launch_bounds__(256) stats_merge_kernel(const double* __restrict__ partial, int nparts,
+static __global__ void __launch_bounds__(256) stats_merge_kernel(const double* __restrict__ partial, int nparts,
                                                           double* __restrict__ out) {
   __shared__ double sc[256], sm[256], s2[256];
   const int row = blockIdx.x;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) stats_merge_kernel(const double* __restri
 }
 
 // Cross-rank merge: gathered [R][rows][3] folded in rank order 0..R−1.
-__global__ void stats_rank_merge_kernel(const double* __restrict__ g, int R, int rows, double* __restrict__ out) {
+static __global__ void stats_rank_merge_kernel(const double* __restrict__ g, int R, int rows, double* __restrict__ out) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   Moments acc{0, 0, 0};
@@ -121,7 +121,7 @@ __global__ void stats_rank_merge_kernel(const double* __restrict__ g, int R, int
   out[row * 3] = acc.c; out[row * 3 + 1] = acc.mean; out[row * 3 + 2] = acc.m2;
 }
 
-__global__ void stats_finalize_kernel(const double* __restrict__ st, int rows, double* __restrict__ mean,
+static __global__ void stats_finalize_kernel(const double* __restrict__ st, int rows, double* __restrict__ mean,
                                       double* __restrict__ var) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;

@@ -82,6 +82,11 @@ def _call(model, alg, dtype=0, N=16, t0=0.0, tf=1.0, dt=1e-3, **o):
     (dict(model="lorenz", alg="tsit5", saveat=[0.5, 1.5]), 6),                    # outside [t0, tf]
     (dict(model="gbm", alg="em", saveat=[0.00015]), 6),                           # off the EM grid
     (dict(model="lorenz", alg="tsit5"), 7),                                        # no workspace
+    (dict(model="gbm", alg="rodas4"), 2),                                          # Rodas4 on an SDE
+    (dict(model="ball", alg="rodas4", adaptive=1, abstol=1e-6), 8),                # events: Tsit5 only (R18)
+    (dict(model="pollu", alg="rodas4", dtype=0), 8),                               # POLLU: fp64 only
+    (dict(model="lorenz", alg="rodas4", adaptive=1, abstol=-1.0), 4),
+    (dict(model="lorenz", alg="rodas4"), 7),                                       # valid up to the workspace
 ])
 def test_validation_statuses(kw, status):
     assert _call(**kw) == status

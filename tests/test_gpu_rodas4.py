@@ -1,0 +1,118 @@
+"""GPU ↔ oracle parity for Rodas4 (GPURodas4; NEXT-2; DESIGN R20)
+through the C ABI (-m gpu). Same bars as Rosenbrock23: fixed step rel ≤ 1e-12
+(fp64) / 1e-5 (fp32); adaptive fp64 final rel ≤ 1e-8 with identical accepted /
+rejected step counts on ≥ 99.9 % of trajectories."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from synth.inputs import make_inputs
+from tests.helpers import gpu, traj_relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL_FIXED = {"f32": 1e-5, "f64": 1e-12}
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("model,tf,dt", [("lorenz", 1.0, 1e-3), ("robertson", 1.0, 1e-3), ("harmonic", 2.0, 0.01),
+                                         ("hires", 10.0, 0.01)])
+def test_rodas4_fixed_parity(model, tf, dt, dtype):
+    N = 1027
+    u0, p = make_inputs(model, "random10", N, seed=0x4D, dtype=dtype)
+    sa = np.array([0.0, tf / 3, tf / 2 + dt / 3, tf])
+    g, rc, na, nr, _ = gpu(model, "rodas4", u0, p, (0.0, tf), dt, saveat=sa)
+    o, orc, ona, _ = oracle.solve(model, "rodas4", u0, p, (0.0, tf), dt, dtype=dtype, saveat=sa)
+    np.testing.assert_array_equal(rc, orc)
+    np.testing.assert_array_equal(na, ona)
+    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
+    assert (g == o).mean() >= 0.99          # canonical order on both sides
+
+
+@pytest.mark.parametrize("refill", [False, True])
+def test_rodas4_robertson_c3_shape(refill):
+    """C3 workload on Rodas4: Robertson ±10 % rates, fp64, tol 1e-8, h0 = 1e-4,
+    100 save points over [0, 1e5]."""
+    N = 1030
+    u0, p = make_inputs("robertson", "random10", N, seed=0xC3, dtype="f64")
+    sa = np.linspace(0.0, 1e5, 100)
+    g, rc, na, nr, _ = gpu("robertson", "rodas4", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
+                           reltol=1e-8, saveat=sa, refill=refill)
+    o, orc, ona, onr = oracle.solve("robertson", "rodas4", u0, p, (0.0, 1e5), 1e-4, dtype="f64", adaptive=True,
+                                    abstol=1e-8, reltol=1e-8, saveat=sa)
+    assert (rc == 0).all() and (orc == 0).all()
+    same = (na == ona) & (nr == onr)
+    assert same.mean() >= 0.999, same.mean()
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+    assert np.abs(g.sum(1) - 1).max() <= 1e-12     # Σy = 1 (linear invariant)
+
+
+def test_rodas4_adaptive_tight_tolerance_lorenz():
+    """north_star adaptive bar at abstol = reltol = 1e-10 (fp64)."""
+    N = 777
+    u0, p = make_inputs("lorenz", "random10", N, seed=0xC1, dtype="f64")
+    g, rc, na, nr, _ = gpu("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10)
+    o, orc, ona, onr = oracle.solve("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
+                                    abstol=1e-10, reltol=1e-10)
+    np.testing.assert_array_equal(rc, orc)
+    same = (na == ona) & (nr == onr)
+    assert same.mean() >= 0.999, same.mean()
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+
+
+@pytest.mark.parametrize("model,tf,N", [("orego", 30.0, 300), ("hires", 321.8122, 500), ("pollu", 60.0, 300)])
+def test_rodas4_stiff_suite_parity(model, tf, N):
+    u0, p = make_inputs(model, "random10", N, seed=0x57, dtype="f64")
+    sa = np.linspace(0.0, tf, 7)
+    g, rc, na, nr, _ = gpu(model, "rodas4", u0, p, (0.0, tf), 1e-6, adaptive=True, abstol=1e-8, reltol=1e-8,
+                           saveat=sa)
+    o, orc, ona, onr = oracle.solve(model, "rodas4", u0, p, (0.0, tf), 1e-6, dtype="f64", adaptive=True,
+                                    abstol=1e-8, reltol=1e-8, saveat=sa)
+    np.testing.assert_array_equal(rc, orc)
+    assert (rc == 0).mean() > 0.99
+    same = (na == ona) & (nr == onr)
+    assert same.mean() >= 0.999, same.mean()
+    ok = (rc == 0) & same
+    assert traj_relerr(g[..., ok], o[..., ok]).max() <= 1e-8
+
+
+def test_rodas4_stiff_references_on_gpu():
+    """GPU Rodas4 on HIRES / POLLU / OREGO against the IVP test-set references."""
+    ref = json.loads((Path(__file__).parent / "golden" / "stiff_references.json").read_text())
+    for model, tol, bound in [("hires", 1e-10, 2e-6), ("pollu", 1e-10, 1e-6), ("orego", 1e-9, 1e-4)]:
+        u0, p = make_inputs(model, "const", 32, dtype="f64")
+        if model == "pollu":
+            u0[8, :] = ref["pollu"]["y9_0"]
+        g, rc, *_ = gpu(model, "rodas4", u0, p, (0.0, ref[model]["tf"]), 1e-6, adaptive=True, abstol=tol,
+                        reltol=tol)
+        assert (rc == 0).all()
+        r = np.array(ref[model]["y"])
+        big = np.abs(r) > 1e-10
+        rel = np.abs(g[0][:, 0] - r)[big] / np.abs(r[big])
+        assert rel.max() < bound, (model, rel.max())
+
+
+def test_rodas4_adaptive_lorenz_f32():
+    N = 513
+    u0, p = make_inputs("lorenz", "random10", N, seed=9, dtype="f32")
+    g, rc, na, *_ = gpu("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
+    o, orc, ona, _ = oracle.solve("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
+                                  abstol=1e-5, reltol=1e-5)
+    same = na == ona
+    assert same.mean() >= 0.99
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-3
+
+
+def test_rodas4_ragged_and_single():
+    """N = 1 and a ragged tail (N = 257) give the oracle's answer."""
+    for N in [1, 257]:
+        u0, p = make_inputs("robertson", "random10", N, seed=3, dtype="f64")
+        g, rc, na, nr, _ = gpu("robertson", "rodas4", u0, p, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-8,
+                               reltol=1e-8)
+        o, orc, ona, onr = oracle.solve("robertson", "rodas4", u0, p, (0.0, 10.0), 1e-4, dtype="f64", adaptive=True,
+                                        abstol=1e-8, reltol=1e-8)
+        np.testing.assert_array_equal(rc, orc)
+        assert traj_relerr(g, o).max() <= 1e-8

@@ -43,7 +43,12 @@ def timeit(fn, reps=5, warm=2):
     return best
 
 
+ONLY: list[str] = []
+
+
 def run(name, model, alg, recipe, N, dtype, tspan, dt, flop_key=None, reps=5, **kw):
+    if ONLY and not any(name.startswith(o) for o in ONLY):
+        return None
     u0, p = ens.generate_inputs(model, recipe, N, dtype=T[dtype], seed=kw.pop("input_seed", 0), N_total=N)
     sa = kw.get("saveat")
     k = 0 if sa is None else len(sa)
@@ -82,7 +87,9 @@ def run(name, model, alg, recipe, N, dtype, tspan, dt, flop_key=None, reps=5, **
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="comma-separated config-name prefixes")
     args = ap.parse_args()
+    ONLY[:] = [o for o in args.only.split(",") if o]
     big = 10**6 if args.quick else 10**7
     # C1: Lorenz N=1024, random p ±10 %, fp64 adaptive 1e-8 (latency regime)
     for refill in [False, True]:
@@ -100,6 +107,10 @@ def main():
     for refill in [False, True]:
         run("C3", "robertson", "rosenbrock23", "random10", 10**6, "f64", (0.0, 1e5), 1e-4, "ros23", reps=3,
             input_seed=0xC3, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa, refill=refill)
+    # NEXT-2: the C3 workload on Rodas4 (4th order: far fewer steps at the same tolerance)
+    for refill in [False, True]:
+        run("C3-rodas4", "robertson", "rodas4", "random10", 10**6, "f64", (0.0, 1e5), 1e-4, None, reps=3,
+            input_seed=0xC3, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa, refill=refill)
     # C4: stochastic Lorenz EM dt=1e-3, 10^6 paths, 11 save points, ensemble mean/var
     sa4 = [j / 10 for j in range(11)]
     for model in ["lorenz_sde_add", "lorenz_sde_mul"]:
@@ -114,6 +125,8 @@ def main():
     # NEXT-4: stiff suite at the paper's 8192 trajectories, Rosenbrock23 fp64, tol 1e-8
     for model, tf in [("orego", 30.0), ("hires", 321.8122), ("pollu", 60.0)]:
         run("stiff-" + model, model, "rosenbrock23", "random10", 8192, "f64", (0.0, tf), 1e-6, "ros23", reps=3,
+            input_seed=0x57, adaptive=True, abstol=1e-8, reltol=1e-8)
+        run("stiff-rodas4-" + model, model, "rodas4", "random10", 8192, "f64", (0.0, tf), 1e-6, None, reps=3,
             input_seed=0x57, adaptive=True, abstol=1e-8, reltol=1e-8)
     # C5: Lorenz fp32 10^8 on one GPU (the 8-GPU run shards this), random p ±10 %
     if not args.quick:
