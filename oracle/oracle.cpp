@@ -40,7 +40,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -1048,6 +1048,143 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
   }
 }
 
+// ----------------------------------------------------------------- Vern7 ----
+// GPUVern7 (NEXT-1). The paper names the method but prints no
+// coefficients; DESIGN R21: Verner's "most efficient" 7(6) pair — nodes c,
+// matrix A and 7th-order weights b as published (pinned by all 85 order-7
+// conditions, tests/test_oracle_vern7.py); the order-6 embedded weights are
+// the one direction the order conditions leave, scaled by b̂1 (derived by
+// tools/derive_vern7_embedded.py); stored as b̃ = b − b̂. Not FSAL: k1 = f(u)
+// is evaluated after each accepted step. Saves: fixed step — grid points only
+// (R11 rule); adaptive — the step is clipped to land on the next save point
+// (R21; the paper's lazy interpolant is not reproduced), so every saved value
+// carries the method's full order.
+static const double V7_C[10] = {0.0, 0.005, 0.10888888888888888, 0.16333333333333333, 0.4555,
+                                0.6095094489978381, 0.884, 0.925, 1.0, 1.0};
+static const double V7_A[10][9] = {
+  {0, 0, 0, 0, 0, 0, 0, 0, 0},
+  {0.005, 0, 0, 0, 0, 0, 0, 0, 0},
+  {-1.07679012345679, 1.185679012345679, 0, 0, 0, 0, 0, 0, 0},
+  {0.04083333333333333, 0, 0.1225, 0, 0, 0, 0, 0, 0},
+  {0.6389139236255726, 0, -2.455672638223657, 2.272258714598084, 0, 0, 0, 0, 0},
+  {-2.6615773750187572, 0, 10.804513886456137, -8.3539146573962, 0.820487594956657, 0, 0, 0, 0},
+  {6.067741434696772, 0, -24.711273635911088, 20.427517930788895, -1.9061579788166472, 1.006172249242068,
+   0, 0, 0},
+  {12.054670076253203, 0, -49.75478495046899, 41.142888638604674, -4.461760149974004, 2.042334822239175,
+   -0.09834843665406107, 0, 0},
+  {10.138146522881808, 0, -42.6411360317175, 35.76384003992257, -4.3480228403929075, 2.0098622683770357,
+   0.3487490460338272, -0.27143900510483127, 0},
+  {-45.030072034298676, 0, 187.3272437654589, -154.02882369350186, 18.56465306347536, -7.141809679295079,
+   1.3088085781613787, 0, 0}};
+static const double V7_B[10] = {0.04715561848627222, 0, 0, 0.25750564298434153, 0.2621665397741262,
+                                0.15216092656738558, 0.4939969170032485, -0.29430311714032503,
+                                0.08131747232495111, 0};
+static const double V7_BT[10] = {0.0030925885828119940, 0, 0, -0.011727248681971966, 0.051075082200004638,
+                                 -0.080965757291055731, 0.32177553732670404, -0.35734362573070983,
+                                 0.098735890663364916, -0.024642467069148059};
+static const Ctrl CTRL_VERN7 = {7.0 / 70.0, 2.0 / 35.0, 0.9, 5.0, 0.1, 1e-4};   // p=7
+
+// One Vern7 step. K[0] = f(u) on entry. Canonical order: stage
+// sums as Tsit5 (fma with h·a_sj rounded to T), terms with a zero coefficient
+// skipped; u_new = u + Σ (h·b_j) k_j in the same fma form; E = h·(Σ b̃_j k_j).
+template <class T>
+static void vern7_step(int model, int n, const T* p, T t, T h, const T* u, T (*K)[NMAX], T* unew, T* E) {
+  T y[NMAX];
+  for (int s = 1; s < 10; ++s) {
+    for (int c = 0; c < n; ++c) {
+      T acc = u[c];
+      for (int j = 0; j < s; ++j)
+        if (V7_A[s][j] != 0.0) acc = std::fma(h * (T)V7_A[s][j], K[j][c], acc);
+      y[c] = acc;
+    }
+    rhs<T>(model, y, p, t, K[s]);
+  }
+  for (int c = 0; c < n; ++c) {
+    T acc = u[c];
+    for (int j = 0; j < 10; ++j)
+      if (V7_B[j] != 0.0) acc = std::fma(h * (T)V7_B[j], K[j][c], acc);
+    unew[c] = acc;
+    if (E) {
+      T e = (T)V7_BT[0] * K[0][c];
+      for (int j = 1; j < 10; ++j)
+        if (V7_BT[j] != 0.0) e = std::fma((T)V7_BT[j], K[j][c], e);
+      E[c] = h * e;
+    }
+  }
+}
+
+template <class T>
+static void solve_vern7(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+  const int n = tr.n, model = o.model;
+  T u[NMAX], K[10][NMAX], unew[NMAX], E[NMAX];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  const int k = o.k;
+  std::vector<T> tau(k);
+  for (int j = 0; j < k; ++j) tau[j] = (T)o.saveat[j];
+  int js = 0;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  T t = (T)o.t0;
+  const T tf = (T)o.tf;
+  rhs<T>(model, u, p, t, K[0]);
+  // saves at t0 (DESIGN R5): fixed step — grid index 0; adaptive — τ ≤ t0
+  if (!o.adaptive) { while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; } }
+  else { while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; } }
+  if (!finite_vec(K[0], n)) {
+    tr.retcode = RET_DIVERGED;
+  } else if (!o.adaptive) {
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    const T hdt = (T)o.dt, hl = (T)h_last;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const bool last = (i == nsteps - 1);
+      const T h = last ? hl : hdt;
+      t = (T)(o.t0 + (double)i * o.dt);
+      vern7_step<T>(model, n, p, t, h, u, K, unew, nullptr);
+      for (int j = 0; j < n; ++j) u[j] = unew[j];
+      const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
+      if (!last) rhs<T>(model, u, p, tn, K[0]);
+      tr.n_accept++;
+      while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
+    }
+    t = tf;
+    if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  } else {
+    const Ctrl& C = CTRL_VERN7;
+    const T abstol = (T)o.abstol, reltol = (T)o.reltol;
+    T h = (T)std::min(o.dt, o.tf - o.t0);
+    T lq_old = (T)L_FLOOR;
+    int64_t attempts = 0;
+    while (t < tf) {
+      if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
+      const T target = (js < k) ? tau[js] : tf;                   // next save point (or tf)
+      const bool clip = (t + h >= target);
+      if (clip) h = target - t;
+      vern7_step<T>(model, n, p, t, h, u, K, unew, E);
+      const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
+      ++attempts;
+      if (q2 < T(1)) {
+        t = clip ? target : t + h;
+        for (int j = 0; j < n; ++j) u[j] = unew[j];
+        if (clip && js < k) { put(tr.save, n, js, u); ++js; }
+        rhs<T>(model, u, p, t, K[0]);
+        tr.n_accept++;
+        h = pi_accept<T>(C, h, q2, &lq_old);
+      } else {
+        h = pi_reject<T>(C, h, q2);
+        tr.n_reject++;
+      }
+      if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
+    }
+  }
+  if (k == 0) put(tr.save, n, 0, u);
+  else {
+    const T nan = std::numeric_limits<T>::quiet_NaN();
+    T nv[NMAX]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    for (; js < k; ++js) put(tr.save, n, js, nv);
+  }
+}
+
 // --------------------------------------------------------- Euler–Maruyama ----
 // u_{i+1} = u_i + h a(u_i,t_i) + b(u_i,t_i) ⊙ ΔW_i, ΔW_i = √h Z_i ~ N(0, h I)
 // (P:153-157). Fixed grid (DESIGN R3); saveat on grid points (DESIGN R11).
@@ -1150,7 +1287,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM || o.alg == SIEA) {
+  if (o.alg == EM || o.alg == SIEA || (o.alg == VERN7 && !o.adaptive)) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
@@ -1169,6 +1306,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     if (o.alg == TSIT5) solve_tsit5<T>(o, tr);
     else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
     else if (o.alg == RODAS4) solve_rodas4<T>(o, tr);
+    else if (o.alg == VERN7) solve_vern7<T>(o, tr, save_step.data());
     else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
     for (int s = 0; s < kk; ++s)
@@ -1219,7 +1357,8 @@ void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
 }
 void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
 static const orc::Ctrl& ctrl_of(int alg) {
-  return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4 : orc::CTRL_TSIT5;
+  return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4
+       : alg == orc::VERN7 ? orc::CTRL_VERN7 : orc::CTRL_TSIT5;
 }
 // Rodas4 tableau export for the order-condition pins: gamma, A[36], C[36] (6×6 row-major, strictly lower), D[10].
 void orc_rodas4_tableau(double* gamma, double* A, double* C, double* D) {
@@ -1230,6 +1369,13 @@ void orc_rodas4_tableau(double* gamma, double* A, double* C, double* D) {
       C[i * 6 + j] = j < 5 ? orc::RD_C[i][j] : 0.0;
     }
   for (int j = 0; j < 5; ++j) { D[j] = orc::RD_D2[j]; D[5 + j] = orc::RD_D3[j]; }
+}
+// Vern7 tableau export for the order-condition pins: c[10], A[100] (10×10 row-major), b[10], btilde[10].
+void orc_vern7_tableau(double* c, double* A, double* b, double* bt) {
+  for (int i = 0; i < 10; ++i) {
+    c[i] = orc::V7_C[i]; b[i] = orc::V7_B[i]; bt[i] = orc::V7_BT[i];
+    for (int j = 0; j < 10; ++j) A[i * 10 + j] = j < 9 ? orc::V7_A[i][j] : 0.0;
+  }
 }
 void orc_controller(int alg, double* out6) {
   const orc::Ctrl& C = ctrl_of(alg);
