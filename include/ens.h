@@ -43,7 +43,8 @@ typedef enum {
   ENS_E_ADAPTIVE_UNSUPPORTED = 3, /* EM with adaptive = 1 ("only supports fixed time-stepping") */
   ENS_E_BAD_TOLERANCE = 4,        /* adaptive with abstol <= 0 or reltol < 0 or non-finite */
   ENS_E_BAD_TSPAN = 5,            /* t0 >= tf, dt <= 0, or a non-finite value */
-  ENS_E_BAD_SAVEAT = 6,           /* saveat not strictly increasing, outside [t0,tf], or off the EM grid */
+  ENS_E_BAD_SAVEAT = 6,           /* saveat not strictly increasing, outside [t0,tf], or off the step grid
+                                     (EM / SIEA / fixed-step Vern7) */
   ENS_E_WORKSPACE = 7,            /* workspace NULL or smaller than ens_workspace_bytes() */
   ENS_E_UNSUPPORTED = 8,          /* valid but not built (e.g. Rosenbrock23 on an SDE model's drift) */
   ENS_E_CUDA = 9                  /* a CUDA runtime call or kernel launch failed */
@@ -78,8 +79,11 @@ typedef enum {
   ENS_ROSENBROCK23 = 1,    /* ode23s Rosenbrock-W 2(3), ode23s interpolant */
   ENS_EM = 2,              /* Euler–Maruyama, fixed step, diagonal or model-defined noise */
   ENS_SIEA = 3,            /* weak order 2.0 stochastic improved Euler, fixed step, diagonal noise (R19) */
-  ENS_RODAS4 = 4           /* 4th-order stiffly accurate Rosenbrock, L-stable, fixed or adaptive (R20);
+  ENS_RODAS4 = 4,          /* 4th-order stiffly accurate Rosenbrock, L-stable, fixed or adaptive (R20);
                               ODE models without events; POLLU fp64 only */
+  ENS_VERN7 = 5            /* Verner 7(6), fixed or adaptive (R21); saves keep full order: fixed
+                              step — saveat on the step grid; adaptive — steps clipped to land on saveat.
+                              ODE models with n <= 8 and no events */
 } ens_alg;
 
 typedef enum { ENS_F32 = 0, ENS_F64 = 1 } ens_dtype;

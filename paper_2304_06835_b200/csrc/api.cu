@@ -50,6 +50,10 @@ bool model_dims(int model, int* n, int* m, int* nw) {
 }
 
 inline bool is_sde_alg(int alg) { return alg == ENS_EM || alg == ENS_SIEA; }
+// save points given as step-grid indices (DESIGN R11; fixed-step Vern7, R21)
+inline bool grid_saves(int alg, const ens_options* opt) {
+  return is_sde_alg(alg) || (alg == ENS_VERN7 && !opt->adaptive);
+}
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // DESIGN R3: fixed-step count and last step, in fp64.
@@ -93,6 +97,7 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_TSIT5: return launch_tsit5<T>(model, a, opt, s);
     case ENS_ROSENBROCK23: return launch_ros23<T>(model, a, opt, s);
     case ENS_RODAS4: return launch_rodas4<T>(model, a, opt, s);
+    case ENS_VERN7: return launch_vern7<T>(model, a, opt, s);
     case ENS_EM: case ENS_SIEA: return launch_sde<T>(model, alg, a, opt, s);
   }
   return ENS_E_INVALID_ARG;
@@ -103,7 +108,7 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
                     const ens_options* opt, int* n_out) {
   int n, m, nw;
   if (!opt || N < 1 || !model_dims(model, &n, &m, &nw)) return ENS_E_INVALID_ARG;
-  if (alg < ENS_TSIT5 || alg > ENS_RODAS4 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (alg < ENS_TSIT5 || alg > ENS_VERN7 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
   const bool sde = nw > 0;
@@ -181,7 +186,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
       for (int j = 0; j < a.k; ++j) tau[j] = (T)opt->saveat[j];
       if (cudaMemcpyAsync(ws + L.tau, tau.data(), sizeof(T) * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return ENS_E_CUDA;
-      if (is_sde_alg(alg)) {
+      if (grid_saves(alg, opt)) {
         std::vector<int64_t> st;
         if (!em_save_steps(t0, tf, dt, opt->saveat, a.k, st)) return ENS_E_BAD_SAVEAT;
         if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -234,7 +239,7 @@ ens_status ensemble_solve(ens_model model, ens_alg alg, ens_dtype dtype, int64_t
   if (!out || !u0 || !p) return ENS_E_INVALID_ARG;
   if (!out->u_out && !(is_sde_alg(alg) && opt->want_stats)) return ENS_E_INVALID_ARG;
   if (opt->want_stats && !out->stats) return ENS_E_INVALID_ARG;
-  if (is_sde_alg(alg) && opt->n_saveat > 0) {
+  if (grid_saves(alg, opt) && opt->n_saveat > 0) {
     std::vector<int64_t> tmp;
     if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
   }
@@ -255,14 +260,12 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   if (opt->want_stats) return ENS_E_UNSUPPORTED;
   if (!u0_host || !p_host || !d_u0 || !d_p || !d_u_out || !u_out_host) return ENS_E_INVALID_ARG;
   const int64_t C = std::max<int64_t>(1, std::min<int64_t>(n_chunks, N));
-  if (is_sde_alg(alg)) {
-    // Philox counters key on the global trajectory index (DESIGN R10): each chunk
-    // shifts index_offset by its start; a block-cyclic map cannot be split that way.
-    if (opt->chunk_len > 0 && C > 1) return ENS_E_UNSUPPORTED;
-    if (opt->n_saveat > 0) {
-      std::vector<int64_t> tmp;
-      if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
-    }
+  // Philox counters key on the global trajectory index (DESIGN R10): each chunk
+  // shifts index_offset by its start; a block-cyclic map cannot be split that way.
+  if (is_sde_alg(alg) && opt->chunk_len > 0 && C > 1) return ENS_E_UNSUPPORTED;
+  if (grid_saves(alg, opt) && opt->n_saveat > 0) {
+    std::vector<int64_t> tmp;
+    if (!em_save_steps(t0, tf, dt, opt->saveat, opt->n_saveat, tmp)) return ENS_E_BAD_SAVEAT;
   }
   if (!workspace || workspace_bytes < ens_workspace_bytes(model, alg, dtype, N, opt)) return ENS_E_WORKSPACE;
   model_dims(model, &n, &m, &nw);

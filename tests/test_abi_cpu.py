@@ -87,6 +87,9 @@ def _call(model, alg, dtype=0, N=16, t0=0.0, tf=1.0, dt=1e-3, **o):
     (dict(model="pollu", alg="rodas4", dtype=0), 8),                               # POLLU: fp64 only
     (dict(model="lorenz", alg="rodas4", adaptive=1, abstol=-1.0), 4),
     (dict(model="lorenz", alg="rodas4"), 7),                                       # valid up to the workspace
+    (dict(model="lorenz", alg="vern7", saveat=[0.00015]), 6),                      # fixed Vern7: grid saves (R21)
+    (dict(model="lorenz", alg="vern7", adaptive=1, abstol=1e-8, saveat=[0.00015]), 7),   # adaptive: any τ
+    (dict(model="gbm", alg="vern7"), 2),
 ])
 def test_validation_statuses(kw, status):
     assert _call(**kw) == status

@@ -1,0 +1,84 @@
+"""GPU ↔ oracle parity for Vern7 (GPUVern7; NEXT-1; DESIGN R21)
+through the C ABI (-m gpu). Bars of BASELINE.json north_star: fixed step rel ≤
+1e-12 (fp64) / 1e-5 (fp32); adaptive fp64 at 1e-10: final rel ≤ 1e-8 and
+identical accepted-step counts on ≥ 99.9 % of trajectories."""
+import numpy as np
+import pytest
+
+import oracle
+from synth.inputs import make_inputs
+from tests.helpers import gpu, traj_relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL_FIXED = {"f32": 1e-5, "f64": 1e-12}
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("model,recipe,tf,dt", [("lorenz", "rho_sweep", 1.0, 1e-3), ("lorenz", "random10", 1.0, 0.01),
+                                                ("harmonic", "random10", 4.0, 0.05)])
+def test_vern7_fixed_parity(model, recipe, tf, dt, dtype):
+    N = 2051
+    u0, p = make_inputs(model, recipe, N, seed=0x77, dtype=dtype)
+    nsteps = int(round(tf / dt))
+    sa = np.array([0.0, dt * (nsteps // 3), dt * (nsteps // 2), tf])      # grid points (R21)
+    g, rc, na, nr, _ = gpu(model, "vern7", u0, p, (0.0, tf), dt, saveat=sa)
+    o, orc, ona, _ = oracle.solve(model, "vern7", u0, p, (0.0, tf), dt, dtype=dtype, saveat=sa)
+    np.testing.assert_array_equal(rc, orc)
+    np.testing.assert_array_equal(na, ona)
+    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
+    assert (g == o).mean() >= 0.99
+
+
+@pytest.mark.parametrize("refill", [False, True])
+def test_vern7_adaptive_tight_tolerance(refill):
+    """north_star adaptive bar (fp64, abstol = reltol = 1e-10) with interior
+    save points hit by step clipping."""
+    N = 1029
+    u0, p = make_inputs("lorenz", "random10", N, seed=0xC1, dtype="f64")
+    sa = np.array([0.0, 0.25, 0.5, 0.8125, 1.0])
+    g, rc, na, nr, _ = gpu("lorenz", "vern7", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10,
+                           saveat=sa, refill=refill)
+    o, orc, ona, onr = oracle.solve("lorenz", "vern7", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
+                                    abstol=1e-10, reltol=1e-10, saveat=sa)
+    np.testing.assert_array_equal(rc, orc)
+    same = (na == ona) & (nr == onr)
+    assert same.mean() >= 0.999, same.mean()
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+
+
+def test_vern7_adaptive_final_only_and_f32():
+    N = 777
+    u0, p = make_inputs("lorenz", "random10", N, seed=5, dtype="f64")
+    g, rc, na, nr, _ = gpu("lorenz", "vern7", u0, p, (0.0, 2.0), 1e-3, adaptive=True, abstol=1e-8, reltol=1e-8)
+    o, orc, ona, onr = oracle.solve("lorenz", "vern7", u0, p, (0.0, 2.0), 1e-3, dtype="f64", adaptive=True,
+                                    abstol=1e-8, reltol=1e-8)
+    same = (na == ona) & (nr == onr)
+    assert same.mean() >= 0.999
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+    u0, p = make_inputs("lorenz", "random10", N, seed=6, dtype="f32")
+    g, rc, na, *_ = gpu("lorenz", "vern7", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
+    o, orc, ona, _ = oracle.solve("lorenz", "vern7", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
+                                  abstol=1e-5, reltol=1e-5)
+    same = na == ona
+    assert same.mean() >= 0.99
+    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-3
+
+
+def test_vern7_ragged_single_and_offgrid_saveat():
+    import torch
+
+    import paper_2304_06835_b200 as ens
+    for N in [1, 257]:
+        u0, p = make_inputs("harmonic", "random10", N, seed=3, dtype="f64")
+        g, rc, *_ = gpu("harmonic", "vern7", u0, p, (0.0, 3.0), 0.1, adaptive=True, abstol=1e-9, reltol=1e-9,
+                        saveat=[1.0, 2.5])
+        o, orc, *_ = oracle.solve("harmonic", "vern7", u0, p, (0.0, 3.0), 0.1, dtype="f64", adaptive=True,
+                                  abstol=1e-9, reltol=1e-9, saveat=[1.0, 2.5])
+        np.testing.assert_array_equal(rc, orc)
+        assert traj_relerr(g, o).max() <= 1e-8
+    u0, p = make_inputs("lorenz", "random10", 8, dtype="f64")
+    with pytest.raises(ens.EnsError) as e:
+        ens.solve("lorenz", "vern7", torch.from_numpy(u0).cuda(), torch.from_numpy(p).cuda(), (0.0, 1.0), 0.1,
+                  saveat=[0.05])
+    assert e.value.status == 6
