@@ -24,7 +24,7 @@ _LIB = _HERE / "liboracle.so"
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
           "expdecay": 5, "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10,
           "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
@@ -57,6 +57,7 @@ def lib() -> ctypes.CDLL:
         L.orc_ros23_consts.argtypes = [vp, vp]
         L.orc_rodas4_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_vern7_tableau.argtypes = [vp, vp, vp, vp]
+        L.orc_rodas5_tableau.argtypes = [vp, vp, vp]
         L.orc_controller.argtypes = [i32, vp]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_pi.argtypes = [i32, i32, dbl, dbl, ctypes.POINTER(dbl)]
@@ -138,6 +139,13 @@ def vern7_tableau():
     c = np.zeros(10); A = np.zeros((10, 10)); b = np.zeros(10); bt = np.zeros(10)
     lib().orc_vern7_tableau(_p(c), _p(A), _p(b), _p(bt))
     return c, A, b, bt
+
+
+def rodas5_tableau():
+    """(gamma, A[8,8], C[8,8]) of Rodas5 in W-form (DESIGN R22)."""
+    g = np.zeros(1); A = np.zeros((8, 8)); C = np.zeros((8, 8))
+    lib().orc_rodas5_tableau(_p(g), _p(A), _p(C))
+    return float(g[0]), A, C
 
 
 def controller(alg: str):

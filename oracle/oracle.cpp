@@ -40,7 +40,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5, RODAS5 = 6 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -1048,6 +1048,142 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
   }
 }
 
+// ---------------------------------------------------------------- Rodas5 ----
+// GPURodas5P's base method (NEXT-2; DESIGN R22): Di Marzo's Rodas5,
+// the 8-stage order-5(4) stiffly accurate W-form Rosenbrock method that
+// Rodas5P re-optimises (Rodas5P's own coefficients are not recoverable
+// offline). Same W-form and conventions as Rodas4: Y7 = Y6 + k6, Y8 = Y7 + k7,
+// u_new = Y8 + k8, E = k8. Pinned by the Rosenbrock B-series order conditions
+// (every rooted tree of order ≤ 5; tests/test_oracle_rodas5.py). No dense
+// output is recoverable either: saves clip the step like Vern7 (R21).
+static const double RD5_GAMMA = 0.19;
+static const double RD5_A[8][7] = {
+  {0, 0, 0, 0, 0, 0, 0},
+  {2.0, 0, 0, 0, 0, 0, 0},
+  {3.040894194418781, 1.041747909077569, 0, 0, 0, 0, 0},
+  {2.576417536461461, 1.622083060776640, -0.9089668560264532, 0, 0, 0, 0},
+  {2.760842080225597, 1.446624659844071, -0.3036980084553738, 0.2877498600325443, 0, 0, 0},
+  {-14.09640773051259, 6.925207756232704, -41.47510893210728, 2.343771018586405, 24.13215229196062, 0, 0},
+  {-14.09640773051259, 6.925207756232704, -41.47510893210728, 2.343771018586405, 24.13215229196062, 1.0, 0},
+  {-14.09640773051259, 6.925207756232704, -41.47510893210728, 2.343771018586405, 24.13215229196062, 1.0, 1.0}};
+static const double RD5_C[8][7] = {
+  {0, 0, 0, 0, 0, 0, 0},
+  {-10.31323885133993, 0, 0, 0, 0, 0, 0},
+  {-21.04823117650003, -7.234992135176716, 0, 0, 0, 0, 0},
+  {32.22751541853323, -4.943732386540191, 19.44922031041879, 0, 0, 0, 0},
+  {-20.69865579590063, -8.816374604402768, 1.260436877740897, -0.7495647613787146, 0, 0, 0},
+  {-46.22004352711257, -17.49534862857472, -289.6389582892057, 93.60855400400906, 318.3822534212147, 0, 0},
+  {34.20013733472935, -14.15535402717690, 57.82335640988400, 25.83362985412365, 1.408950972071624,
+   -6.551835421242162, 0},
+  {42.57076742291101, -13.80770672017997, 93.98938432427124, 18.77919633714503, -31.58359187223370,
+   -6.685968952921985, -5.810979938412932}};
+static const Ctrl CTRL_RODAS5 = {7.0 / 50.0, 2.0 / 25.0, 0.9, 5.0, 0.1, 1e-4};   // p=5
+
+// One Rodas5 step (autonomous models). F0 = f(u). Outputs u_new, E = k8.
+template <class T>
+static bool rodas5_step(int model, int n, const T* p, T t, T h, const T* u, const T* F0, T* unew, T* E) {
+  T J[NMAX * NMAX], W[NMAX * NMAX], inv[NMAX]; int piv[NMAX];
+  T K[8][NMAX];
+  jac<T>(model, u, p, t, J);
+  const T hg = h * (T)RD5_GAMMA;
+  const T ihg = T(1) / hg;                                             // 1/(hγ)
+  const T ih = T(1) / h;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) W[i * n + j] = (i == j ? ihg : T(0)) - J[i * n + j];   // W = I/(hγ) − J
+  if (!lu_factor<T>(n, W, piv, inv)) return false;
+  lu_solve<T>(n, W, piv, inv, F0, K[0]);                               // k1 = W⁻¹ f(u)
+  T y[NMAX], F[NMAX], r[NMAX];
+  for (int s = 1; s < 8; ++s) {
+    for (int c = 0; c < n; ++c) {                                      // Y_s = u + Σ_{j<s} a_sj k_j
+      T acc = u[c];
+      for (int j = 0; j < s; ++j) acc = std::fma((T)RD5_A[s][j], K[j][c], acc);
+      y[c] = acc;
+    }
+    rhs<T>(model, y, p, t, F);
+    for (int c = 0; c < n; ++c) {                                      // f(Y_s) + Σ_{j<s} (c_sj/h) k_j
+      T acc = F[c];
+      for (int j = 0; j < s; ++j) acc = std::fma((T)RD5_C[s][j] * ih, K[j][c], acc);
+      r[c] = acc;
+    }
+    lu_solve<T>(n, W, piv, inv, r, K[s]);
+  }
+  for (int c = 0; c < n; ++c) { unew[c] = y[c] + K[7][c]; E[c] = K[7][c]; }   // u_new = Y8 + k8
+  return true;
+}
+
+template <class T>
+static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+  const int n = tr.n, model = o.model;
+  const Ctrl& C = CTRL_RODAS5;
+  T u[NMAX], F0[NMAX], unew[NMAX], E[NMAX];
+  for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
+  const T* p = tr.p;
+  const int k = o.k;
+  std::vector<T> tau(k);
+  for (int j = 0; j < k; ++j) tau[j] = (T)o.saveat[j];
+  int js = 0;
+  tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
+  T t = (T)o.t0;
+  const T tf = (T)o.tf, abstol = (T)o.abstol, reltol = (T)o.reltol;
+  rhs<T>(model, u, p, t, F0);
+  if (!o.adaptive) { while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; } }
+  else { while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; } }
+  if (!finite_vec(F0, n)) tr.retcode = RET_DIVERGED;
+  else if (!o.adaptive) {
+    int64_t nsteps; double h_last;
+    fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
+    const T hdt = (T)o.dt, hl = (T)h_last;
+    for (int64_t i = 0; i < nsteps; ++i) {
+      const bool last = (i == nsteps - 1);
+      const T h = last ? hl : hdt;
+      t = (T)(o.t0 + (double)i * o.dt);
+      if (!rodas5_step<T>(model, n, p, t, h, u, F0, unew, E)) { tr.retcode = RET_SINGULAR; break; }
+      for (int j = 0; j < n; ++j) u[j] = unew[j];
+      if (!last) rhs<T>(model, u, p, (T)(o.t0 + (double)(i + 1) * o.dt), F0);
+      tr.n_accept++;
+      while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
+    }
+    t = tf;
+    if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
+  } else {
+    T h = (T)std::min(o.dt, o.tf - o.t0);
+    T lq_old = (T)L_FLOOR;
+    int64_t attempts = 0;
+    while (t < tf) {
+      if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
+      const T target = (js < k) ? tau[js] : tf;                   // next save point (or tf), R21 rule
+      const bool clip = (t + h >= target);
+      if (clip) h = target - t;
+      ++attempts;
+      if (!rodas5_step<T>(model, n, p, t, h, u, F0, unew, E)) {
+        h = h * T(0.5);                                   // singular W: reject, halve (DESIGN R10)
+        tr.n_reject++;
+        if (t + h == t) { tr.retcode = RET_SINGULAR; break; }
+        continue;
+      }
+      const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
+      if (q2 < T(1)) {
+        t = clip ? target : t + h;
+        for (int j = 0; j < n; ++j) u[j] = unew[j];
+        if (clip && js < k) { put(tr.save, n, js, u); ++js; }
+        rhs<T>(model, u, p, t, F0);
+        tr.n_accept++;
+        h = pi_accept<T>(C, h, q2, &lq_old);
+      } else {
+        h = pi_reject<T>(C, h, q2);
+        tr.n_reject++;
+      }
+      if (t < tf && t + h == t) { tr.retcode = RET_DTMIN; break; }
+    }
+  }
+  if (k == 0) put(tr.save, n, 0, u);
+  else {
+    const T nan = std::numeric_limits<T>::quiet_NaN();
+    T nv[NMAX]; for (int j = 0; j < n; ++j) nv[j] = nan;
+    for (; js < k; ++js) put(tr.save, n, js, nv);
+  }
+}
+
 // ----------------------------------------------------------------- Vern7 ----
 // GPUVern7 (NEXT-1). The paper names the method but prints no
 // coefficients; DESIGN R21: Verner's "most efficient" 7(6) pair — nodes c,
@@ -1287,7 +1423,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM || o.alg == SIEA || (o.alg == VERN7 && !o.adaptive)) {
+  if (o.alg == EM || o.alg == SIEA || ((o.alg == VERN7 || o.alg == RODAS5) && !o.adaptive)) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
@@ -1307,6 +1443,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
     else if (o.alg == RODAS4) solve_rodas4<T>(o, tr);
     else if (o.alg == VERN7) solve_vern7<T>(o, tr, save_step.data());
+    else if (o.alg == RODAS5) solve_rodas5<T>(o, tr, save_step.data());
     else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
     for (int s = 0; s < kk; ++s)
@@ -1358,7 +1495,7 @@ void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
 void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
 static const orc::Ctrl& ctrl_of(int alg) {
   return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4
-       : alg == orc::VERN7 ? orc::CTRL_VERN7 : orc::CTRL_TSIT5;
+       : alg == orc::VERN7 ? orc::CTRL_VERN7 : alg == orc::RODAS5 ? orc::CTRL_RODAS5 : orc::CTRL_TSIT5;
 }
 // Rodas4 tableau export for the order-condition pins: gamma, A[36], C[36] (6×6 row-major, strictly lower), D[10].
 void orc_rodas4_tableau(double* gamma, double* A, double* C, double* D) {
@@ -1376,6 +1513,15 @@ void orc_vern7_tableau(double* c, double* A, double* b, double* bt) {
     c[i] = orc::V7_C[i]; b[i] = orc::V7_B[i]; bt[i] = orc::V7_BT[i];
     for (int j = 0; j < 10; ++j) A[i * 10 + j] = j < 9 ? orc::V7_A[i][j] : 0.0;
   }
+}
+// Rodas5 tableau export: gamma, A[64], C[64] (8×8 row-major, strictly lower).
+void orc_rodas5_tableau(double* gamma, double* A, double* C) {
+  *gamma = orc::RD5_GAMMA;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      A[i * 8 + j] = j < 7 ? orc::RD5_A[i][j] : 0.0;
+      C[i * 8 + j] = j < 7 ? orc::RD5_C[i][j] : 0.0;
+    }
 }
 void orc_controller(int alg, double* out6) {
   const orc::Ctrl& C = ctrl_of(alg);

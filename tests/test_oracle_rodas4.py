@@ -190,3 +190,16 @@ def test_rodas4_adaptive_tolerance_proportionality():
         assert rc[0] == 0
         errs.append(np.abs(out[0, :, 0] - ref[0, :, 0]).max() / np.abs(ref[0, :, 0]).max())
     assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-6, errs
+
+
+def test_rodas4_full_bseries_order():
+    """Every rooted tree up to order 5 through the general Rosenbrock B-series
+    recursion (tests/order_conditions.py): main order exactly 4, embedded 3."""
+    from tests.order_conditions import rosenbrock_residuals
+    g, A, C, D = oracle.rodas4_tableau()
+    m = np.concatenate([A[5, :5], [1.0]])
+    me = np.concatenate([A[5, :5], [0.0]])
+    r = rosenbrock_residuals(A, C, g, m, 5)
+    assert max(r[k] for k in range(1, 5)) < 1e-13 and r[5] > 1e-4, r
+    r = rosenbrock_residuals(A, C, g, me, 4)
+    assert max(r[k] for k in range(1, 4)) < 1e-13 and r[4] > 1e-3, r

@@ -1,65 +1,22 @@
 """Pins for the oracle's Vern7 (GPUVern7; NEXT-1; DESIGN R21).
 
-The tableau is checked against Butcher's rooted-tree order conditions generated
-here from scratch (all 85 trees of order ≤ 7 for b, all 37 of order ≤ 6 for the
+The tableau is checked against Butcher's rooted-tree order conditions
+(tests/order_conditions.py) (all 85 trees of order ≤ 7 for b, all 37 of order ≤ 6 for the
 embedded b̂ = b − b̃), against measured convergence orders on a closed-form and a
 nonlinear problem, and the saveat rule (step clipping) against plain runs to the
 same end time.
 """
 import math
-from functools import lru_cache
 
 import numpy as np
 import pytest
 
 import oracle
-
-
-@lru_cache(None)
-def _trees(n):
-    """Rooted trees with n nodes, as sorted tuples of child trees."""
-    if n == 1:
-        return ((),)
-    out = set()
-
-    def gen(rem, maxkey, acc):
-        if rem == 0:
-            out.add(tuple(sorted(acc)))
-            return
-        for k in range(1, rem + 1):
-            for t in _trees(k):
-                if maxkey is not None and (k, t) > maxkey:
-                    continue
-                gen(rem - k, (k, t), acc + [t])
-    gen(n - 1, None, [])
-    return tuple(sorted(out))
-
-
-def _size(t):
-    return 1 + sum(_size(c) for c in t)
-
-
-def _gamma(t):
-    g = _size(t)
-    for c in t:
-        g *= _gamma(c)
-    return g
-
-
-def _phi(t, A):
-    v = np.ones(A.shape[0])
-    for ch in t:
-        v = v * (A @ _phi(ch, A))
-    return v
+from tests.order_conditions import rk_max_residual
 
 
 def _max_residual(b, A, order):
-    return max(abs(b @ _phi(t, A) - 1.0 / _gamma(t)) for t in _trees(order))
-
-
-def test_tree_enumeration():
-    """Number of rooted trees of order 1..8 (OEIS A000081)."""
-    assert [len(_trees(n)) for n in range(1, 9)] == [1, 1, 2, 4, 9, 20, 48, 115]
+    return rk_max_residual(b, A, order)
 
 
 def test_vern7_order_conditions():
