@@ -1,7 +1,7 @@
 // k_rodas4.cu — Rodas4 kernel instances (fixed step; adaptive static or
 // refill) for the ODE models without events.
 #include "launch.cuh"
-#include "rodas4.cuh"
+#include "rodas.cuh"
 
 namespace ens {
 

@@ -1,0 +1,35 @@
+// k_rodas5.cu — Rodas5 kernel instances (R22; fixed step with grid saves;
+// adaptive static or refill with step-clipped saves) for the ODE models without events.
+#include "launch.cuh"
+#include "rodas.cuh"
+
+namespace ens {
+
+template <class M, class T>
+ens_status run_rodas5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  const bool save = a.k > 0;
+  if (!opt->adaptive) {
+    const dim3 g = grid_for(a.N), b(solver_block(a.N));
+    if (save) rodas_grid_fixed_kernel<Rodas5Tab, M, T, true><<<g, b, 0, s>>>(a);
+    else rodas_grid_fixed_kernel<Rodas5Tab, M, T, false><<<g, b, 0, s>>>(a);
+  } else {
+    if (save) launch_adaptive<RodasClipLane<Rodas5Tab, M, T, true>, T>(a, opt->refill, s);
+    else launch_adaptive<RodasClipLane<Rodas5Tab, M, T, false>, T>(a, opt->refill, s);
+  }
+  return launch_status();
+}
+
+template <class T>
+ens_status launch_rodas5(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
+  return with_ode_model(model, [&](auto mt) -> ens_status {
+    using M = decltype(mt);
+    if constexpr (HasEvent<M>::value) return ENS_E_UNSUPPORTED;                  // events: Tsit5 only (R18)
+    else if constexpr (M::n > 8 && sizeof(T) == 4) return ENS_E_UNSUPPORTED;     // POLLU: fp64 only
+    else return run_rodas5<M, T>(a, opt, s);
+  });
+}
+
+template ens_status launch_rodas5<float>(int, const Args<float>&, const ens_options*, cudaStream_t);
+template ens_status launch_rodas5<double>(int, const Args<double>&, const ens_options*, cudaStream_t);
+
+}  // namespace ens

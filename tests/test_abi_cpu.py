@@ -90,6 +90,8 @@ def _call(model, alg, dtype=0, N=16, t0=0.0, tf=1.0, dt=1e-3, **o):
     (dict(model="lorenz", alg="vern7", saveat=[0.00015]), 6),                      # fixed Vern7: grid saves (R21)
     (dict(model="lorenz", alg="vern7", adaptive=1, abstol=1e-8, saveat=[0.00015]), 7),   # adaptive: any τ
     (dict(model="gbm", alg="vern7"), 2),
+    (dict(model="lorenz", alg="rodas5", saveat=[0.00015]), 6),                     # fixed Rodas5: grid saves (R22)
+    (dict(model="ball", alg="rodas5", adaptive=1, abstol=1e-6), 8),
 ])
 def test_validation_statuses(kw, status):
     assert _call(**kw) == status
