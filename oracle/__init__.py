@@ -24,7 +24,7 @@ _LIB = _HERE / "liboracle.so"
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
           "expdecay": 5, "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10,
           "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6, "vern9": 7}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
@@ -58,6 +58,7 @@ def lib() -> ctypes.CDLL:
         L.orc_rodas4_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_vern7_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_rodas5_tableau.argtypes = [vp, vp, vp]
+        L.orc_vern9_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_controller.argtypes = [i32, vp]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_pi.argtypes = [i32, i32, dbl, dbl, ctypes.POINTER(dbl)]
@@ -138,6 +139,13 @@ def vern7_tableau():
     """(c[10], A[10,10], b[10], btilde[10]) of Vern7 (DESIGN R21)."""
     c = np.zeros(10); A = np.zeros((10, 10)); b = np.zeros(10); bt = np.zeros(10)
     lib().orc_vern7_tableau(_p(c), _p(A), _p(b), _p(bt))
+    return c, A, b, bt
+
+
+def vern9_tableau():
+    """(c[16], A[16,16], b[16], btilde[16]) of Vern9 (DESIGN R21)."""
+    c = np.zeros(16); A = np.zeros((16, 16)); b = np.zeros(16); bt = np.zeros(16)
+    lib().orc_vern9_tableau(_p(c), _p(A), _p(b), _p(bt))
     return c, A, b, bt
 
 

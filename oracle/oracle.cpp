@@ -40,7 +40,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5, RODAS5 = 6 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5, RODAS5 = 6, VERN9 = 7 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -1184,16 +1184,17 @@ static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   }
 }
 
-// ----------------------------------------------------------------- Vern7 ----
-// GPUVern7 (NEXT-1). The paper names the method but prints no
-// coefficients; DESIGN R21: Verner's "most efficient" 7(6) pair — nodes c,
-// matrix A and 7th-order weights b as published (pinned by all 85 order-7
-// conditions, tests/test_oracle_vern7.py); the order-6 embedded weights are
-// the one direction the order conditions leave, scaled by b̂1 (derived by
-// tools/derive_vern7_embedded.py); stored as b̃ = b − b̂. Not FSAL: k1 = f(u)
+// ---------------------------------------------------------- Vern7 / Vern9 ----
+// GPUVern7 / GPUVern9 (NEXT-1). The paper names the methods but
+// prints no coefficients; DESIGN R21: Verner's "most efficient" 7(6) and 9(8)
+// pairs — nodes c, matrix A and weights b as published (pinned by every
+// rooted-tree condition of order ≤ 7 / ≤ 9, tests/test_oracle_vern7.py,
+// tests/test_oracle_vern9.py); the embedded weights are the one direction the
+// order conditions leave, scaled by the published b̂1
+// (tools/derive_verner_embedded.py); stored as b̃ = b − b̂. Not FSAL: k1 = f(u)
 // is evaluated after each accepted step. Saves: fixed step — grid points only
 // (R11 rule); adaptive — the step is clipped to land on the next save point
-// (R21; the paper's lazy interpolant is not reproduced), so every saved value
+// (R21; the paper's lazy interpolants are not reproduced), so every saved value
 // carries the method's full order.
 static const double V7_C[10] = {0.0, 0.005, 0.10888888888888888, 0.16333333333333333, 0.4555,
                                 0.6095094489978381, 0.884, 0.925, 1.0, 1.0};
@@ -1218,41 +1219,92 @@ static const double V7_B[10] = {0.04715561848627222, 0, 0, 0.25750564298434153, 
 static const double V7_BT[10] = {0.0030925885828119940, 0, 0, -0.011727248681971966, 0.051075082200004638,
                                  -0.080965757291055731, 0.32177553732670404, -0.35734362573070983,
                                  0.098735890663364916, -0.024642467069148059};
+static const double V9_C[16] = {0.0, 0.03462, 0.09702435063878045, 0.14553652595817068, 0.561,
+                                0.22900791159048503, 0.544992088409515, 0.645, 0.48375, 0.06757, 0.25,
+                                0.6590650618730999, 0.8206, 0.9012, 1.0, 1.0};
+static const double V9_A[16][15] = {
+  {0},
+  {0.03462},
+  {-0.0389335438857287, 0.13595789452451916},
+  {0.03638413148954267, 0, 0.10915239446862801},
+  {2.0257639143939694, 0, -7.638023836496292, 6.173259922102322},
+  {0.05112275589406061, 0, 0, 0.17708237945550218, 0.0008027762409222536},
+  {0.13160063579752163, 0, 0, -0.2957276252669636, 0.08781378035642955, 0.6213052975225274},
+  {0.07166666666666667, 0, 0, 0, 0, 0.33055335789153195, 0.2427799754418014},
+  {0.071806640625, 0, 0, 0, 0, 0.3294380283228177, 0.1165190029271823, -0.034013671875},
+  {0.04836757646340646, 0, 0, 0, 0, 0.03928989925676164, 0.10547409458903446, -0.021438652846483126,
+   -0.10412291746271944},
+  {-0.026645614872014785, 0, 0, 0, 0, 0.03333333333333333, -0.1631072244872467, 0.03396081684127761,
+   0.1572319413814626, 0.21522674780318796},
+  {0.03689009248708622, 0, 0, 0, 0, -0.1465181576725543, 0.2242577768172024, 0.02294405717066073,
+   -0.0035850052905728597, 0.08669223316444385, 0.43838406519683376},
+  {-0.4866012215113341, 0, 0, 0, 0, -6.304602650282853, -0.2812456182894729, -2.679019236219849,
+   0.5188156639241577, 1.3653531876033418, 5.8850910885039465, 2.8028087862720628},
+  {0.4185367457753472, 0, 0, 0, 0, 6.724547581906459, -0.42544428016461133, 3.3432791530012653,
+   0.6170816631175374, -0.9299661239399329, -6.099948804751011, -3.002206187889399, 0.2553202529443446},
+  {-0.7793740861228848, 0, 0, 0, 0, -13.937342538107776, 1.2520488533793563, -14.691500408016868,
+   -0.494705058533141, 2.2429749091462368, 13.367893803828643, 14.396650486650687, -0.79758133317768,
+   0.4409353709534278},
+  {2.0580513374668867, 0, 0, 0, 0, 22.357937727968032, 0.9094981099755646, 35.89110098240264,
+   -3.442515027624454, -4.865481358036369, -18.909803813543427, -34.26354448030452, 1.2647565216956427}};
+static const double V9_B[16] = {0.014611976858423152, 0, 0, 0, 0, 0, 0, -0.3915211862331339,
+                                0.23109325002895065, 0.12747667699928525, 0.2246434176204158,
+                                0.5684352689748513, 0.058258715572158275, 0.13643174034822156,
+                                0.030570139830827976, 0};
+static const double V9_BT[16] = {-0.0053579882904445780, 0, 0, 0, 0, 0, 0, -2.5830204911777926,
+                                 0.14252253154675679, 0.013420653512693399, -0.028672962914105127,
+                                 2.6249996552108000, -0.28255096432831926, 0.13643174034775387,
+                                 0.030570139830719485, -0.048342313738061889};
 static const Ctrl CTRL_VERN7 = {7.0 / 70.0, 2.0 / 35.0, 0.9, 5.0, 0.1, 1e-4};   // p=7
+static const Ctrl CTRL_VERN9 = {7.0 / 90.0, 2.0 / 45.0, 0.9, 5.0, 0.1, 1e-4};   // p=9
 
-// One Vern7 step. K[0] = f(u) on entry. Canonical order: stage
+struct VernTab {
+  int S;              // stages
+  const double* A;    // S rows of lda entries: a_sj (j < s)
+  int lda;
+  const double* B;    // b_j
+  const double* BT;   // b̃_j = b_j − b̂_j
+  const Ctrl* ctrl;
+};
+static const VernTab VERN7_TAB = {10, &V7_A[0][0], 9, V7_B, V7_BT, &CTRL_VERN7};
+static const VernTab VERN9_TAB = {16, &V9_A[0][0], 15, V9_B, V9_BT, &CTRL_VERN9};
+
+// One Verner step. K[0] = f(u) on entry. Canonical order: stage
 // sums as Tsit5 (fma with h·a_sj rounded to T), terms with a zero coefficient
 // skipped; u_new = u + Σ (h·b_j) k_j in the same fma form; E = h·(Σ b̃_j k_j).
 template <class T>
-static void vern7_step(int model, int n, const T* p, T t, T h, const T* u, T (*K)[NMAX], T* unew, T* E) {
+static void verner_step(const VernTab& tb, int model, int n, const T* p, T t, T h, const T* u, T (*K)[NMAX],
+                        T* unew, T* E) {
   T y[NMAX];
-  for (int s = 1; s < 10; ++s) {
+  for (int s = 1; s < tb.S; ++s) {
     for (int c = 0; c < n; ++c) {
       T acc = u[c];
-      for (int j = 0; j < s; ++j)
-        if (V7_A[s][j] != 0.0) acc = std::fma(h * (T)V7_A[s][j], K[j][c], acc);
+      for (int j = 0; j < s; ++j) {
+        const double a = tb.A[s * tb.lda + j];
+        if (a != 0.0) acc = std::fma(h * (T)a, K[j][c], acc);
+      }
       y[c] = acc;
     }
     rhs<T>(model, y, p, t, K[s]);
   }
   for (int c = 0; c < n; ++c) {
     T acc = u[c];
-    for (int j = 0; j < 10; ++j)
-      if (V7_B[j] != 0.0) acc = std::fma(h * (T)V7_B[j], K[j][c], acc);
+    for (int j = 0; j < tb.S; ++j)
+      if (tb.B[j] != 0.0) acc = std::fma(h * (T)tb.B[j], K[j][c], acc);
     unew[c] = acc;
     if (E) {
-      T e = (T)V7_BT[0] * K[0][c];
-      for (int j = 1; j < 10; ++j)
-        if (V7_BT[j] != 0.0) e = std::fma((T)V7_BT[j], K[j][c], e);
+      T e = (T)tb.BT[0] * K[0][c];
+      for (int j = 1; j < tb.S; ++j)
+        if (tb.BT[j] != 0.0) e = std::fma((T)tb.BT[j], K[j][c], e);
       E[c] = h * e;
     }
   }
 }
 
 template <class T>
-static void solve_vern7(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const int n = tr.n, model = o.model;
-  T u[NMAX], K[10][NMAX], unew[NMAX], E[NMAX];
+  T u[NMAX], K[16][NMAX], unew[NMAX], E[NMAX];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
   const int k = o.k;
@@ -1276,7 +1328,7 @@ static void solve_vern7(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
       const bool last = (i == nsteps - 1);
       const T h = last ? hl : hdt;
       t = (T)(o.t0 + (double)i * o.dt);
-      vern7_step<T>(model, n, p, t, h, u, K, unew, nullptr);
+      verner_step<T>(tb, model, n, p, t, h, u, K, unew, nullptr);
       for (int j = 0; j < n; ++j) u[j] = unew[j];
       const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
       if (!last) rhs<T>(model, u, p, tn, K[0]);
@@ -1286,7 +1338,7 @@ static void solve_vern7(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
     t = tf;
     if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;
   } else {
-    const Ctrl& C = CTRL_VERN7;
+    const Ctrl& C = *tb.ctrl;
     const T abstol = (T)o.abstol, reltol = (T)o.reltol;
     T h = (T)std::min(o.dt, o.tf - o.t0);
     T lq_old = (T)L_FLOOR;
@@ -1296,7 +1348,7 @@ static void solve_vern7(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
       const T target = (js < k) ? tau[js] : tf;                   // next save point (or tf)
       const bool clip = (t + h >= target);
       if (clip) h = target - t;
-      vern7_step<T>(model, n, p, t, h, u, K, unew, E);
+      verner_step<T>(tb, model, n, p, t, h, u, K, unew, E);
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
       if (q2 < T(1)) {
@@ -1423,7 +1475,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM || o.alg == SIEA || ((o.alg == VERN7 || o.alg == RODAS5) && !o.adaptive)) {
+  if (o.alg == EM || o.alg == SIEA || ((o.alg == VERN7 || o.alg == VERN9 || o.alg == RODAS5) && !o.adaptive)) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
@@ -1442,7 +1494,8 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     if (o.alg == TSIT5) solve_tsit5<T>(o, tr);
     else if (o.alg == ROSENBROCK23) solve_ros23<T>(o, tr);
     else if (o.alg == RODAS4) solve_rodas4<T>(o, tr);
-    else if (o.alg == VERN7) solve_vern7<T>(o, tr, save_step.data());
+    else if (o.alg == VERN7) solve_verner<T>(VERN7_TAB, o, tr, save_step.data());
+    else if (o.alg == VERN9) solve_verner<T>(VERN9_TAB, o, tr, save_step.data());
     else if (o.alg == RODAS5) solve_rodas5<T>(o, tr, save_step.data());
     else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
@@ -1495,7 +1548,8 @@ void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
 void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
 static const orc::Ctrl& ctrl_of(int alg) {
   return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4
-       : alg == orc::VERN7 ? orc::CTRL_VERN7 : alg == orc::RODAS5 ? orc::CTRL_RODAS5 : orc::CTRL_TSIT5;
+       : alg == orc::VERN7 ? orc::CTRL_VERN7 : alg == orc::RODAS5 ? orc::CTRL_RODAS5
+       : alg == orc::VERN9 ? orc::CTRL_VERN9 : orc::CTRL_TSIT5;
 }
 // Rodas4 tableau export for the order-condition pins: gamma, A[36], C[36] (6×6 row-major, strictly lower), D[10].
 void orc_rodas4_tableau(double* gamma, double* A, double* C, double* D) {
@@ -1522,6 +1576,13 @@ void orc_rodas5_tableau(double* gamma, double* A, double* C) {
       A[i * 8 + j] = j < 7 ? orc::RD5_A[i][j] : 0.0;
       C[i * 8 + j] = j < 7 ? orc::RD5_C[i][j] : 0.0;
     }
+}
+// Vern9 tableau export: c[16], A[256] (16×16 row-major), b[16], btilde[16].
+void orc_vern9_tableau(double* c, double* A, double* b, double* bt) {
+  for (int i = 0; i < 16; ++i) {
+    c[i] = orc::V9_C[i]; b[i] = orc::V9_B[i]; bt[i] = orc::V9_BT[i];
+    for (int j = 0; j < 16; ++j) A[i * 16 + j] = j < 15 ? orc::V9_A[i][j] : 0.0;
+  }
 }
 void orc_controller(int alg, double* out6) {
   const orc::Ctrl& C = ctrl_of(alg);
