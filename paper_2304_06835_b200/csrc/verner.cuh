@@ -1,8 +1,9 @@
-// vern7.cuh — per-thread Vern7 explicit 7(6) integrator for sm_100a (GPUVern7,
-// P:319-320; NEXT-1; DESIGN R21).
+// verner.cuh — per-thread Verner explicit integrators for sm_100a: Vern7
+// (10-stage 7(6)) and Vern9 (16-stage 9(8)) — GPUVern7 / GPUVern9,
+// P:319-320; NEXT-1; DESIGN R21.
 //
-// Verner's 10-stage 7th-order pair; the embedded order-6 weights are derived
-// from the order conditions (R21). All ten stage vectors stay in registers;
+// Verner's pairs; the embedded weights are derived from the order conditions
+// (R21). All stage vectors stay in registers;
 // zero tableau entries are compile-time constants, so their terms vanish from
 // the instruction stream. Saves keep the full order (R21): fixed step — on
 // grid points; adaptive — the step is clipped to land on the next save point.
@@ -42,20 +43,78 @@ __host__ __device__ constexpr double v7_bt(int j) {   // b − b̂ (R21)
   return BT[j];
 }
 
-// K[0] = f(u) on entry; fills K[1..9], u_new and (if WANT_E) E = h·Σ b̃_j k_j.
-template <class M, class T, bool WANT_E>
-__device__ __forceinline__ void vern7_step(const T (&par)[M::m], T t, T h, const T (&u)[M::n], T (&K)[10][M::n],
-                                           T (&un)[M::n], T (&E)[M::n]) {
-  constexpr int n = M::n;
+__host__ __device__ constexpr double v9_a(int s, int j) {
+  constexpr double A[16][15] = {
+      {0},
+      {0.03462},
+      {-0.0389335438857287, 0.13595789452451916},
+      {0.03638413148954267, 0, 0.10915239446862801},
+      {2.0257639143939694, 0, -7.638023836496292, 6.173259922102322},
+      {0.05112275589406061, 0, 0, 0.17708237945550218, 0.0008027762409222536},
+      {0.13160063579752163, 0, 0, -0.2957276252669636, 0.08781378035642955, 0.6213052975225274},
+      {0.07166666666666667, 0, 0, 0, 0, 0.33055335789153195, 0.2427799754418014},
+      {0.071806640625, 0, 0, 0, 0, 0.3294380283228177, 0.1165190029271823, -0.034013671875},
+      {0.04836757646340646, 0, 0, 0, 0, 0.03928989925676164, 0.10547409458903446, -0.021438652846483126,
+       -0.10412291746271944},
+      {-0.026645614872014785, 0, 0, 0, 0, 0.03333333333333333, -0.1631072244872467, 0.03396081684127761,
+       0.1572319413814626, 0.21522674780318796},
+      {0.03689009248708622, 0, 0, 0, 0, -0.1465181576725543, 0.2242577768172024, 0.02294405717066073,
+       -0.0035850052905728597, 0.08669223316444385, 0.43838406519683376},
+      {-0.4866012215113341, 0, 0, 0, 0, -6.304602650282853, -0.2812456182894729, -2.679019236219849,
+       0.5188156639241577, 1.3653531876033418, 5.8850910885039465, 2.8028087862720628},
+      {0.4185367457753472, 0, 0, 0, 0, 6.724547581906459, -0.42544428016461133, 3.3432791530012653,
+       0.6170816631175374, -0.9299661239399329, -6.099948804751011, -3.002206187889399, 0.2553202529443446},
+      {-0.7793740861228848, 0, 0, 0, 0, -13.937342538107776, 1.2520488533793563, -14.691500408016868,
+       -0.494705058533141, 2.2429749091462368, 13.367893803828643, 14.396650486650687, -0.79758133317768,
+       0.4409353709534278},
+      {2.0580513374668867, 0, 0, 0, 0, 22.357937727968032, 0.9094981099755646, 35.89110098240264,
+       -3.442515027624454, -4.865481358036369, -18.909803813543427, -34.26354448030452, 1.2647565216956427}};
+  return j < 15 ? A[s][j] : 0.0;
+}
+__host__ __device__ constexpr double v9_b(int j) {
+  constexpr double B[16] = {0.014611976858423152, 0, 0, 0, 0, 0, 0, -0.3915211862331339, 0.23109325002895065,
+                            0.12747667699928525, 0.2246434176204158, 0.5684352689748513, 0.058258715572158275,
+                            0.13643174034822156, 0.030570139830827976, 0};
+  return B[j];
+}
+__host__ __device__ constexpr double v9_bt(int j) {   // b − b̂ (R21)
+  constexpr double BT[16] = {-0.0053579882904445780, 0, 0, 0, 0, 0, 0, -2.5830204911777926, 0.14252253154675679,
+                             0.013420653512693399, -0.028672962914105127, 2.6249996552108000,
+                             -0.28255096432831926, 0.13643174034775387, 0.030570139830719485,
+                             -0.048342313738061889};
+  return BT[j];
+}
+
+// Tableau traits: S stages, a / b / b̃, PI exponents (R2 rule with p = order).
+struct Vern7Tab {
+  static constexpr int S = 10;
+  static constexpr double beta1 = 7.0 / 70.0, beta2 = 2.0 / 35.0;
+  __host__ __device__ static constexpr double a(int s, int j) { return j < 9 ? v7_a(s, j) : 0.0; }
+  __host__ __device__ static constexpr double b(int j) { return v7_b(j); }
+  __host__ __device__ static constexpr double bt(int j) { return v7_bt(j); }
+};
+struct Vern9Tab {
+  static constexpr int S = 16;
+  static constexpr double beta1 = 7.0 / 90.0, beta2 = 2.0 / 45.0;
+  __host__ __device__ static constexpr double a(int s, int j) { return v9_a(s, j); }
+  __host__ __device__ static constexpr double b(int j) { return v9_b(j); }
+  __host__ __device__ static constexpr double bt(int j) { return v9_bt(j); }
+};
+
+// K[0] = f(u) on entry; fills K[1..S−1], u_new and (if WANT_E) E = h·Σ b̃_j k_j.
+template <class Tab, class M, class T, bool WANT_E>
+__device__ __forceinline__ void verner_step(const T (&par)[M::m], T t, T h, const T (&u)[M::n],
+                                            T (&K)[Tab::S][M::n], T (&un)[M::n], T (&E)[M::n]) {
+  constexpr int n = M::n, S = Tab::S;
 #pragma unroll
-  for (int s = 1; s < 10; ++s) {
+  for (int s = 1; s < S; ++s) {
     T y[n];
 #pragma unroll
     for (int c = 0; c < n; ++c) {
       T acc = u[c];
 #pragma unroll
       for (int j = 0; j < s; ++j)
-        if (v7_a(s, j) != 0.0) acc = fmaT(h * T(v7_a(s, j)), K[j][c], acc);
+        if (Tab::a(s, j) != 0.0) acc = fmaT(h * T(Tab::a(s, j)), K[j][c], acc);
       y[c] = acc;
     }
     M::f(y, par, t, K[s]);
@@ -64,20 +123,20 @@ __device__ __forceinline__ void vern7_step(const T (&par)[M::m], T t, T h, const
   for (int c = 0; c < n; ++c) {
     T acc = u[c];
 #pragma unroll
-    for (int j = 0; j < 10; ++j)
-      if (v7_b(j) != 0.0) acc = fmaT(h * T(v7_b(j)), K[j][c], acc);
+    for (int j = 0; j < S; ++j)
+      if (Tab::b(j) != 0.0) acc = fmaT(h * T(Tab::b(j)), K[j][c], acc);
     un[c] = acc;
     if (WANT_E) {
-      T e = T(v7_bt(0)) * K[0][c];
+      T e = T(Tab::bt(0)) * K[0][c];
 #pragma unroll
-      for (int j = 1; j < 10; ++j)
-        if (v7_bt(j) != 0.0) e = fmaT(T(v7_bt(j)), K[j][c], e);
+      for (int j = 1; j < S; ++j)
+        if (Tab::bt(j) != 0.0) e = fmaT(T(Tab::bt(j)), K[j][c], e);
       E[c] = h * e;
     }
   }
 }
 
-template <class M, class T, bool SAVE> struct Vern7Lane {
+template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
@@ -102,10 +161,10 @@ template <class M, class T, bool SAVE> struct Vern7Lane {
     const T target = (SAVE && js < a.k) ? __ldg(a.tau + js) : a.tf;   // next save point or tf (R21)
     const bool clip = (t + h >= target);
     if (clip) h = target - t;
-    T K[10][n], un[n], E[n];
+    T K[Tab::S][n], un[n], E[n];
 #pragma unroll
     for (int c = 0; c < n; ++c) K[0][c] = F0[c];
-    vern7_step<M, T, true>(par, t, h, u, K, un, E);
+    verner_step<Tab, M, T, true>(par, t, h, u, K, un, E);
     const T q2 = error_q2<n, T>(E, u, un, a.abstol, a.reltol);
     ++attempts;
     if (q2 < T(1)) {
@@ -115,9 +174,9 @@ template <class M, class T, bool SAVE> struct Vern7Lane {
       if (SAVE && clip && js < a.k) { store_point<n>(a, i, js, u); ++js; }
       M::f(u, par, t, F0);
       ++nacc;
-      h = pi_accept<T>(h, q2, lq_old, 7.0 / 70.0, 2.0 / 35.0);
+      h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
     } else {
-      h = pi_reject<T>(h, q2, 7.0 / 70.0);
+      h = pi_reject<T>(h, q2, Tab::beta1);
       ++nrej;
     }
     if (!(t < a.tf)) done = true;
@@ -139,9 +198,9 @@ template <class M, class T, bool SAVE> struct Vern7Lane {
   }
 };
 
-// Fixed-step Vern7 on the DESIGN R3 grid; saves at grid indices a.save_step.
-template <class M, class T, bool SAVE>
-__global__ void __launch_bounds__(256) vern7_fixed_kernel(const Args<T> a) {
+// Fixed-step Verner on the DESIGN R3 grid; saves at grid indices a.save_step.
+template <class Tab, class M, class T, bool SAVE>
+__global__ void __launch_bounds__(256) verner_fixed_kernel(const Args<T> a) {
   constexpr int n = M::n;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
@@ -159,10 +218,10 @@ __global__ void __launch_bounds__(256) vern7_fixed_kernel(const Args<T> a) {
       const bool last = (s == a.nsteps - 1);
       const T h = last ? a.h_last : a.dt0;
       const T t = (T)(a.t0d + (double)s * a.dtd);
-      T K[10][n], un[n], E[n];
+      T K[Tab::S][n], un[n], E[n];
 #pragma unroll
       for (int c = 0; c < n; ++c) K[0][c] = F0[c];
-      vern7_step<M, T, false>(par, t, h, u, K, un, E);
+      verner_step<Tab, M, T, false>(par, t, h, u, K, un, E);
 #pragma unroll
       for (int c = 0; c < n; ++c) u[c] = un[c];
       if (!last) M::f(u, par, (T)(a.t0d + (double)(s + 1) * a.dtd), F0);

@@ -96,10 +96,11 @@ def main():
         run("C1", "lorenz", "tsit5", "random10", 1024, "f64", (0.0, 1.0), 1e-3, "tsit5_adaptive", reps=20,
             input_seed=0xC1, adaptive=True, abstol=1e-8, reltol=1e-8, refill=refill)
     # NEXT-1: C1 on Vern7, and Tsit5 vs Vern7 at the north_star's tight fp64 tolerance (1e-10)
-    for refill in [False, True]:
-        run("C1-vern7", "lorenz", "vern7", "random10", 1024, "f64", (0.0, 1.0), 1e-3, None, reps=20,
-            input_seed=0xC1, adaptive=True, abstol=1e-8, reltol=1e-8, refill=refill)
-    for alg in ["tsit5", "vern7"]:
+    for alg in ["vern7", "vern9"]:
+        for refill in [False, True]:
+            run("C1-" + alg, "lorenz", alg, "random10", 1024, "f64", (0.0, 1.0), 1e-3, None, reps=20,
+                input_seed=0xC1, adaptive=True, abstol=1e-8, reltol=1e-8, refill=refill)
+    for alg in ["tsit5", "vern7", "vern9"]:
         run("tight-" + alg, "lorenz", alg, "rho_sweep", 10**6, "f64", (0.0, 1.0), 1e-3, None, reps=3,
             adaptive=True, abstol=1e-10, reltol=1e-10, refill=True)
     run("C2-fixed-vern7", "lorenz", "vern7", "rho_sweep", big, "f32", (0.0, 1.0), 1e-3, None)
