@@ -10,7 +10,8 @@
  *
  * Conventions (all entry points):
  *  - extern "C"; no exceptions cross the ABI; no global mutable state (only
- *    cached device attributes). Every status is returned, never thrown.
+ *    cached device attributes and per-kernel block-size choices, mutex
+ *    guarded). Every status is returned, never thrown.
  *  - Device buffers are caller-owned (allocated by PyTorch or cudaMalloc); the
  *    library allocates nothing on the device. Host buffers are caller-owned.
  *  - Layout is structure-of-arrays, trajectory fastest: element (trajectory i,

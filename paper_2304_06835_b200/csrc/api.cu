@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/ens.h"
@@ -27,6 +29,21 @@ int ens::sm_count() {
     if (cached <= 0) cached = 148;
   }
   return cached;
+}
+
+// Occupancy-tuned block sizes (launch.cuh::occupancy_block), cached per (kernel, start size).
+namespace {
+std::mutex g_block_mu;
+std::map<std::pair<const void*, int>, int> g_block_cache;
+}  // namespace
+int ens::cached_block(const void* kernel, int b0) {
+  std::lock_guard<std::mutex> lk(g_block_mu);
+  const auto it = g_block_cache.find({kernel, b0});
+  return it == g_block_cache.end() ? 0 : it->second;
+}
+void ens::cache_block(const void* kernel, int b0, int b) {
+  std::lock_guard<std::mutex> lk(g_block_mu);
+  g_block_cache[{kernel, b0}] = b;
 }
 
 namespace {

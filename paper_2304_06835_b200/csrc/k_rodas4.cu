@@ -9,9 +9,8 @@ template <class M, class T>
 ens_status run_rodas4(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
   if (!opt->adaptive) {
-    const dim3 g = grid_for(a.N), b(solver_block(a.N));
-    if (save) rodas4_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
-    else rodas4_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    if (save) launch_fixed(rodas4_fixed_kernel<M, T, true>, a, s);
+    else launch_fixed(rodas4_fixed_kernel<M, T, false>, a, s);
   } else {
     if (save) launch_adaptive<Rodas4Lane<M, T, true>, T>(a, opt->refill, s);
     else launch_adaptive<Rodas4Lane<M, T, false>, T>(a, opt->refill, s);

@@ -11,9 +11,8 @@ template <class M, class T>
 ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
   if (!opt->adaptive) {
-    const dim3 g = grid_for(a.N), b(solver_block(a.N));
-    if (save) ros23_fixed_kernel<M, T, true><<<g, b, 0, s>>>(a);
-    else ros23_fixed_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    if (save) launch_fixed(ros23_fixed_kernel<M, T, true>, a, s);
+    else launch_fixed(ros23_fixed_kernel<M, T, false>, a, s);
   } else {
     // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
     // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log). ENS_TUNE_ROS23_MINB=1 reverts.

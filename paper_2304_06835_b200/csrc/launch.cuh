@@ -31,22 +31,55 @@ inline int solver_block(int64_t threads) {
 }
 inline dim3 grid_for(int64_t N) { return dim3((unsigned)cdiv(N, solver_block(N))); }
 
+// Register-heavy kernels (fp64 Vern9 / Rodas5 / Vern7: 120–140 registers) fit
+// only one or two 256-thread blocks per SM; smaller blocks pack more warps into
+// the same register file. Starting from solver_block(N), pick the block size
+// (256 / 128 / 64) with the most resident warps per SM (ties: the larger).
+// Results do not depend on it (one trajectory per thread).
+int cached_block(const void* kernel, int b0);          // api.cu: 0 if not cached yet
+void cache_block(const void* kernel, int b0, int b);    // api.cu
+
+template <class K>
+int occupancy_block(K kernel, int64_t N) {
+  const int b0 = solver_block(N);
+  if (const int c = cached_block((const void*)kernel, b0)) return c;
+  int best_b = b0, best_w = -1;
+  for (int b = b0; b >= 64; b /= 2) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, b, 0) != cudaSuccess) break;
+    const int w = occ * (b / 32);
+    if (w > best_w) { best_w = w; best_b = b; }
+    if (b == b0 && occ * b >= 2048) break;   // already full residency
+  }
+  cache_block((const void*)kernel, b0, best_b);
+  return best_b;
+}
+
 inline ens_status launch_status() { return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA; }
 
 // Adaptive solve of one lane type: static mapping (one trajectory per thread)
 // or the a8 refill scheduler with a grid of exactly the resident warps.
 template <class Lane, class T, int MINB = 1>
 void launch_adaptive(const Args<T>& a, bool refill, cudaStream_t s) {
-  const dim3 b(solver_block(a.N));
   if (refill) {
     auto kern = adaptive_refill_kernel<Lane, T>;
+    const dim3 b(occupancy_block(kern, a.N));
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
     const dim3 gr((unsigned)std::min<int64_t>(cdiv(a.N, b.x), (int64_t)std::max(1, occ) * sm_count()));
     kern<<<gr, b, 0, s>>>(a);
   } else {
-    adaptive_static_kernel<Lane, T, MINB><<<grid_for(a.N), b, 0, s>>>(a);
+    auto kern = adaptive_static_kernel<Lane, T, MINB>;
+    const dim3 b(occupancy_block(kern, a.N));
+    kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
   }
+}
+
+// One-thread-per-trajectory launch of a fixed-step kernel with the occupancy-tuned block.
+template <class K, class T>
+void launch_fixed(K kern, const Args<T>& a, cudaStream_t s) {
+  const dim3 b(occupancy_block(kern, a.N));
+  kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
 }
 
 // ODE model dispatch: calls f(M{}) with the model type for `model`.

@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Run one config a few times (for ncu capture). Usage: prof_one.py NAME [N]
 NAME: c2a (Lorenz tsit5 adaptive fp32 1e-6 rho sweep), c3 (Robertson ros23 fp64
-saveat 100), c4 (stochastic Lorenz EM fp32 stats), c1 (Lorenz fp64 adaptive 1e-8)."""
+saveat 100), c3r5 (the same on Rodas5), c4 (stochastic Lorenz EM fp32 stats),
+c4d (the same fp64), c1 (Lorenz fp64 adaptive 1e-8), tight9 / tight7 (Lorenz fp64
+1e-10 on Vern9 / Vern7, refill)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -25,6 +27,24 @@ elif name == "c3":
     sa = [1e5 * j / 99 for j in range(100)]
     f = lambda: ens.solve("robertson", "rosenbrock23", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                           reltol=1e-8, saveat=sa)
+elif name == "c3r5":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("robertson", "random10", N, dtype=torch.float64, seed=0xC3)
+    sa = [1e5 * j / 99 for j in range(100)]
+    f = lambda: ens.solve("robertson", "rodas5", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
+                          reltol=1e-8, saveat=sa)
+elif name in ("tight9", "tight7"):
+    N = N or 10**6
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float64, N_total=N)
+    alg = "vern9" if name == "tight9" else "vern7"
+    f = lambda: ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10,
+                          refill=True)
+elif name == "c4d":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("lorenz_sde_add", "const", N, dtype=torch.float64)
+    sa = [j / 10 for j in range(11)]
+    f = lambda: ens.solve("lorenz_sde_add", "em", u0, p, (0.0, 1.0), 1e-3, seed=0xC4, saveat=sa, stats=True,
+                          store_states=False)
 elif name == "c4":
     N = N or 10**6
     u0, p = ens.generate_inputs("lorenz_sde_add", "const", N, dtype=torch.float32)
