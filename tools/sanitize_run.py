@@ -28,6 +28,15 @@ for dt in [torch.float32, torch.float64]:
               saveat=np.linspace(0, 10, 4))
     ens.solve("robertson", "rosenbrock23", ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6,
               refill=True)
+    for alg in ["rodas4", "rodas5"]:
+        ens.solve("robertson", alg, ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6,
+                  saveat=np.linspace(0, 10, 4))
+        ens.solve("robertson", alg, ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True)
+        ens.solve("robertson", alg, ur, pr, (0.0, 1.0), 0.01, saveat=[0.0, 0.5, 1.0])
+    for alg in ["vern7", "vern9"]:
+        ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, saveat=sa)
+        ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True)
+        ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, saveat=[0.0, 0.5, 1.0])
     us, ps = ens.generate_inputs("lorenz_sde_mul", "const", N, dtype=dt)
     ens.solve("lorenz_sde_mul", "em", us, ps, (0.0, 0.1), 1e-3, seed=5, saveat=np.linspace(0, 0.1, 3), stats=True,
               store_states=False)
@@ -44,7 +53,11 @@ uh, ph = ens.generate_inputs("hires", "random10", 64, dtype=torch.float64, seed=
 ens.solve("hires", "rosenbrock23", uh, ph, (0.0, 5.0), 1e-6, adaptive=True, abstol=1e-6, reltol=1e-6)
 up, pp = ens.generate_inputs("pollu", "random10", 40, dtype=torch.float64, seed=4)
 ens.solve("pollu", "rosenbrock23", up, pp, (0.0, 1.0), 1e-6, adaptive=True, abstol=1e-6, reltol=1e-6)
+ens.solve("pollu", "rodas5", up, pp, (0.0, 1.0), 1e-6, adaptive=True, abstol=1e-6, reltol=1e-6)
+ens.solve("hires", "rodas4", uh, ph, (0.0, 5.0), 1e-6, adaptive=True, abstol=1e-6, reltol=1e-6, saveat=[1.0, 2.0])
 u0h, p0h = (t.cpu().pin_memory() for t in ens.generate_inputs("lorenz", "random10", N, dtype=torch.float32))
 ens.solve_host("lorenz", "tsit5", u0h, p0h, (0.0, 1.0), 1e-2, n_chunks=3)
+ush, psh = (t.cpu().pin_memory() for t in ens.generate_inputs("gbm", "random10", N, dtype=torch.float64))
+ens.solve_host("gbm", "em", ush, psh, (0.0, 1.0), 1e-2, n_chunks=3, seed=3, index_offset=100)
 torch.cuda.synchronize()
 print("SANITIZE_RUN_OK")
