@@ -197,7 +197,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   a.tau = (const T*)(ws + L.tau);
   a.save_step = (const int64_t*)(ws + L.save_step);
   a.u_out = (T*)out->u_out; a.retcode = out->retcode; a.nacc = out->n_accept; a.nrej = out->n_reject;
-  a.seed = opt->seed; a.index_offset = opt->index_offset; a.chunk_len = opt->chunk_len;
+  a.seed = opt->seed; a.rk = philox_round_keys(opt->seed); a.index_offset = opt->index_offset; a.chunk_len = opt->chunk_len;
   a.chunk_stride = opt->chunk_stride;
   a.partial = (double*)(ws + L.partial);
   a.counter = (unsigned long long*)(ws + L.counter);
@@ -450,11 +450,11 @@ ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step
   const dim3 g((unsigned)cdiv(N, kBlock));
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == ENS_F32) {
-    if (nw == 3) sde_noise_kernel<float, 3><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
-    else sde_noise_kernel<float, 8><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (float*)z);
+    if (nw == 3) sde_noise_kernel<float, 3><<<g, kBlock, 0, s>>>(philox_round_keys(seed), N, step0, nsteps, off, cl, cs, words, (float*)z);
+    else sde_noise_kernel<float, 8><<<g, kBlock, 0, s>>>(philox_round_keys(seed), N, step0, nsteps, off, cl, cs, words, (float*)z);
   } else {
-    if (nw == 3) sde_noise_kernel<double, 3><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
-    else sde_noise_kernel<double, 8><<<g, kBlock, 0, s>>>(seed, N, step0, nsteps, off, cl, cs, words, (double*)z);
+    if (nw == 3) sde_noise_kernel<double, 3><<<g, kBlock, 0, s>>>(philox_round_keys(seed), N, step0, nsteps, off, cl, cs, words, (double*)z);
+    else sde_noise_kernel<double, 8><<<g, kBlock, 0, s>>>(philox_round_keys(seed), N, step0, nsteps, off, cl, cs, words, (double*)z);
   }
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
