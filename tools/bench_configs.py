@@ -50,6 +50,9 @@ def run(name, model, alg, recipe, N, dtype, tspan, dt, flop_key=None, reps=5, **
     if ONLY and not any(name.startswith(o) for o in ONLY):
         return None
     u0, p = ens.generate_inputs(model, recipe, N, dtype=T[dtype], seed=kw.pop("input_seed", 0), N_total=N)
+    if kw.pop("shuffle", False):
+        perm = torch.randperm(N, generator=torch.Generator().manual_seed(1)).cuda()
+        u0, p = u0[:, perm].contiguous(), (p[:, perm].contiguous() if p.dim() == 2 else p)
     sa = kw.get("saveat")
     k = 0 if sa is None else len(sa)
     n = u0.shape[0]
@@ -111,6 +114,11 @@ def main():
             run("C2-adaptive", "lorenz", "tsit5", "rho_sweep", N, "f32", (0.0, 1.0), 1e-3, "tsit5_adaptive",
                 adaptive=True, abstol=1e-6, reltol=1e-6, refill=refill)
     run("C2-fixed", "lorenz", "tsit5", "rho_sweep", big, "f64", (0.0, 1.0), 1e-3, "tsit5_fixed")
+    # the C2 adaptive ensemble with its columns randomly permuted: neighbouring lanes no longer have
+    # similar step counts (20-47), the divergence the refill scheduler (a8) is for
+    for refill in [False, True]:
+        run("C2-adaptive-shuffled", "lorenz", "tsit5", "rho_sweep", big, "f32", (0.0, 1.0), 1e-3, "tsit5_adaptive",
+            adaptive=True, abstol=1e-6, reltol=1e-6, refill=refill, shuffle=True)
     # C3: Robertson N=10^6 fp64 Rosenbrock23 adaptive 1e-8, saveat 100 points (2.4 GB of states)
     sa = [1e5 * j / 99 for j in range(100)]
     for refill in [False, True]:

@@ -17,6 +17,15 @@ if name == "c2a":
     N = N or 10**7
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float32, N_total=N)
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6)
+elif name in ("c2a_refill", "c2a_shuf", "c2a_shuf_refill"):
+    N = N or 10**7
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float32, N_total=N)
+    if "shuf" in name:
+        perm = torch.randperm(N, generator=torch.Generator().manual_seed(1)).cuda()
+        u0, p = u0[:, perm].contiguous(), p[:, perm].contiguous()
+    rf = name.endswith("refill")
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6,
+                          refill=rf)
 elif name == "c1":
     N = N or 1024
     u0, p = ens.generate_inputs("lorenz", "random10", N, dtype=torch.float64, seed=0xC1)
