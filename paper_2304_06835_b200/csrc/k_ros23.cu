@@ -15,12 +15,14 @@ ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
     else launch_fixed(ros23_fixed_kernel<M, T, false>, a, s);
   } else {
     // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
-    // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log). ENS_TUNE_ROS23_MINB=1 reverts.
+    // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log) — for small systems
+    // only: HIRES (n = 8) spills under the cap and runs 17 % slower (profiles/ros23_minb_models_r01.log).
+    // A cap of 4 blocks (64 regs) spills on C3 as well and is slower. ENS_TUNE_ROS23_MINB=1 reverts.
     static const int minb = [] {
       const char* e = getenv("ENS_TUNE_ROS23_MINB");
       return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
     }();
-    if (minb == 3 && !opt->refill) {
+    if (minb == 3 && M::n <= 4 && !opt->refill) {
       if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
       else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
     } else {
