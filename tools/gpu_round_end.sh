@@ -1,0 +1,26 @@
+#!/bin/bash
+# Full evidence refresh (one GPU session): GPU tests, smoke, bench (N=1, default
+# flags), the reference (oracle) arm, torchrun world 1, the ncu launch list of the
+# bench command and one `ncu --set full` capture of the headline kernel.
+# Usage (from the repo root, under gpurun): bash tools/gpu_round_end.sh TAG
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+export PYTHONUNBUFFERED=1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu_$TAG.txt 2>&1
+python -m paper_2304_06835_b200._build > $OUT/build_$TAG.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/pytest_gpu_$TAG.log 2>&1
+echo "pytest rc=$?" >> $OUT/pytest_gpu_$TAG.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1
+echo "smoke rc=$?" >> $OUT/smoke_$TAG.log
+timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
+echo "bench rc=$?" >> $OUT/bench_$TAG.err
+timeout 900 python bench.py --impl reference > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+  --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 > $OUT/bench_torchrun1_$TAG.json 2> $OUT/bench_torchrun1_$TAG.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launch_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tsit5_fixed -s 1 -c 1 \
+  -o $OUT/prof_tsit5_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full_$TAG.log 2>&1
+echo done
