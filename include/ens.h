@@ -191,13 +191,16 @@ ens_status ens_stats_finalize(const double* stats, int32_t k, int32_t n, double*
 ens_status ens_stats_merge(const double* gathered, int32_t R, int32_t k, int32_t n, double* merged,
                            void* stream);
 
-/* SDE noise stream of the EM kernel (DESIGN R8), exposed for verification:
- * Philox4x32-10 words and the nw Box–Muller normals (nw = 3 or 8) that
- * trajectory i (global index per opt's index_offset / chunk fields) draws at
- * steps step0 .. step0+nsteps−1 under key `seed`. words: device uint32
- * [nsteps][4·calls][N] (calls = ceil(nw/4) for F32, ceil(nw/2) for F64) or
- * NULL; z: device T [nsteps][nw][N] or NULL. Same device functions as
- * ensemble_solve. ENS_E_UNSUPPORTED for other nw. */
+/* SDE noise stream of the EM / SIEA kernels (DESIGN R8), exposed for
+ * verification. Trajectory i (global index g per opt's index_offset / chunk
+ * fields) reads one normal stream Z_0, Z_1, …: Philox4x32-10 call c (counter
+ * (c lo, g lo, g hi, c hi), key `seed`) yields PER = 4 (F32) or 2 (F64)
+ * normals, and step s uses Z_{nw·s} … Z_{nw·s+nw−1} (nw = 3 or 8).
+ * z: device T [nsteps][nw][N], the normals of steps step0 .. step0+nsteps−1,
+ * or NULL. words: device uint32 [ncalls][4][N], the raw words of calls
+ * c0 .. c0+ncalls−1 with c0 = floor(nw·step0 / PER) and
+ * ncalls = ceil(nw·(step0+nsteps) / PER) − c0, or NULL. Same device functions
+ * as ensemble_solve. ENS_E_UNSUPPORTED for other nw. */
 ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step0, int64_t nsteps, int32_t nw,
                          const ens_options* opt, uint32_t* words, void* z, void* stream);
 

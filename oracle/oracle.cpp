@@ -424,41 +424,60 @@ template <class T> static T bm_radius(T U) {
   return std::sqrt((T)(-2.0 * 0.693147180559945309417232121458176568) * log2_spec<T>(U));
 }
 
-// nw standard normals for (trajectory gidx, step): Box–Muller pairs in order
-// from Philox calls c = 0, 1, … with counter = (step, gidx lo, gidx hi, c) and
-// key = (seed lo, seed hi) (DESIGN R8). fp32: each call gives two pairs
-// (U0,U1), (U2,U3); fp64: each call gives one pair (U_a from words 0,1; U_b
-// from words 2,3). Each pair gives (R·cos, R·sin); surplus normals are dropped.
-template <class T> static void normalsN(uint64_t seed, uint64_t step, uint64_t gidx, int nw, T* z);
-template <> void normalsN<float>(uint64_t seed, uint64_t step, uint64_t gidx, int nw, float* z) {
+// The normal stream of trajectory gidx (DESIGN R8): Z_0, Z_1, … where Philox
+// call c — counter = (c lo, gidx lo, gidx hi, c hi), key = (seed lo, seed hi) —
+// yields fp32: Z_{4c..4c+3} = (R0·cos θ0, R0·sin θ0, R1·cos θ1, R1·sin θ1) from
+// the Box–Muller pairs (U0,U1), (U2,U3); fp64: Z_{2c}, Z_{2c+1} = (R·cos θ, R·sin θ)
+// from U_a (words 0,1), U_b (words 2,3). Step s of a model with nw Wiener
+// increments uses Z_{nw·s}, …, Z_{nw·s+nw−1}: no normal is drawn and dropped.
+template <class T> struct PerCall;
+template <> struct PerCall<float> { static constexpr int value = 4; };
+template <> struct PerCall<double> { static constexpr int value = 2; };
+
+static void call_words(uint64_t seed, uint64_t gidx, uint64_t c, uint32_t w[4]) {
   const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  for (int c = 0; 4 * c < nw; ++c) {
-    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)c};
-    uint32_t w[4]; philox4x32_10(ctr, key, w);
-    float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
-    for (int q = 0; q < 2; ++q) {
-      const int id = 4 * c + 2 * q;
-      if (id >= nw) break;
-      float sn, cs;
-      const float R = bm_radius<float>(U[2 * q]);
-      sincospi_spec<float>(2.0f * U[2 * q + 1], &sn, &cs);
-      z[id] = R * cs;
-      if (id + 1 < nw) z[id + 1] = R * sn;
-    }
+  const uint32_t ctr[4] = {(uint32_t)c, (uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)(c >> 32)};
+  philox4x32_10(ctr, key, w);
+}
+template <class T> static void call_normals(uint64_t seed, uint64_t gidx, uint64_t c, T* zc);
+template <> void call_normals<float>(uint64_t seed, uint64_t gidx, uint64_t c, float* zc) {
+  uint32_t w[4]; call_words(seed, gidx, c, w);
+  float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
+  for (int q = 0; q < 2; ++q) {
+    float sn, cs;
+    const float R = bm_radius<float>(U[2 * q]);
+    sincospi_spec<float>(2.0f * U[2 * q + 1], &sn, &cs);
+    zc[2 * q] = R * cs;
+    zc[2 * q + 1] = R * sn;
   }
 }
-template <> void normalsN<double>(uint64_t seed, uint64_t step, uint64_t gidx, int nw, double* z) {
-  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  for (int c = 0; 2 * c < nw; ++c) {
-    const uint32_t ctr[4] = {(uint32_t)step, (uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)c};
-    uint32_t w[4]; philox4x32_10(ctr, key, w);
-    const double Ua = u01_f64(w[0], w[1]), Ub = u01_f64(w[2], w[3]);
-    double sn, cs;
-    const double R = bm_radius<double>(Ua);
-    sincospi_spec<double>(2.0 * Ub, &sn, &cs);
-    z[2 * c] = R * cs;
-    if (2 * c + 1 < nw) z[2 * c + 1] = R * sn;
+template <> void call_normals<double>(uint64_t seed, uint64_t gidx, uint64_t c, double* zc) {
+  uint32_t w[4]; call_words(seed, gidx, c, w);
+  const double Ua = u01_f64(w[0], w[1]), Ub = u01_f64(w[2], w[3]);
+  double sn, cs;
+  const double R = bm_radius<double>(Ua);
+  sincospi_spec<double>(2.0 * Ub, &sn, &cs);
+  zc[0] = R * cs;
+  zc[1] = R * sn;
+}
+
+// Z_j of one trajectory's stream, remembering the last Philox call's normals
+// (a trajectory reads its stream in order, so each call is evaluated once).
+template <class T> struct NormalStream {
+  uint64_t seed, gidx;
+  int64_t cached = -1;
+  T zc[4];
+  T at(uint64_t j) {
+    const int per = PerCall<T>::value;
+    const int64_t c = (int64_t)(j / per);
+    if (c != cached) { call_normals<T>(seed, gidx, (uint64_t)c, zc); cached = c; }
+    return zc[j % per];
   }
+};
+
+// nw standard normals of step `step`: Z_{nw·step + q}, q < nw.
+template <class T> static void normalsN(NormalStream<T>& st, uint64_t step, int nw, T* z) {
+  for (int q = 0; q < nw; ++q) z[q] = st.at((uint64_t)nw * step + (uint64_t)q);
 }
 
 // ------------------------------------------------------ fixed-step grid ----
@@ -1389,6 +1408,7 @@ static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
   const T hdt = (T)o.dt, hl = (T)h_last;
   const T sq_dt = std::sqrt(hdt), sq_l = std::sqrt(hl);
+  NormalStream<T> stream{o.seed, tr.gidx};
   int js = 0;
   const int k = o.k;
   tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
@@ -1398,7 +1418,7 @@ static void solve_em(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
     const T h = last ? hl : hdt, sh = last ? sq_l : sq_dt;
     const T t = (T)(o.t0 + (double)i * o.dt);
     rhs<T>(model, u, p, t, a);
-    normalsN<T>(o.seed, (uint64_t)i, tr.gidx, nw, z);
+    normalsN<T>(stream, (uint64_t)i, nw, z);
     for (int q = 0; q < nw; ++q) dW[q] = sh * z[q];              // ΔW = √h Z
     for (int j = 0; j < n; ++j) x[j] = std::fma(h, a[j], u[j]);   // u + h a
     noise_update<T>(model, u, p, t, dW, x);                       // + G ΔW
@@ -1429,6 +1449,7 @@ static void solve_siea(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const T hdt = (T)o.dt, hl = (T)h_last;
   const T sq_dt = std::sqrt(hdt), sq_l = std::sqrt(hl);
   const T isq_dt = T(1) / sq_dt, isq_l = T(1) / sq_l;
+  NormalStream<T> stream{o.seed, tr.gidx};
   int js = 0;
   const int k = o.k;
   tr.retcode = RET_SUCCESS; tr.n_accept = 0; tr.n_reject = 0;
@@ -1439,7 +1460,7 @@ static void solve_siea(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
     const T t = (T)(o.t0 + (double)i * o.dt);
     rhs<T>(model, u, p, t, a);
     diffusion<T>(model, u, p, t, b);
-    normalsN<T>(o.seed, (uint64_t)i, tr.gidx, n, z);
+    normalsN<T>(stream, (uint64_t)i, n, z);
     for (int j = 0; j < n; ++j) {
       dW[j] = sh * z[j];
       const T base = std::fma(h, a[j], u[j]);              // u + a h
@@ -1618,9 +1639,11 @@ void orc_uniforms(int dtype, const uint32_t* w4, void* out) {
 }
 // Normals for `count` consecutive steps of trajectory gidx: out[count][3].
 void orc_normals(int dtype, uint64_t seed, uint64_t gidx, int64_t step0, int64_t count, int nw, void* out) {
+  orc::NormalStream<float> sf{seed, gidx};
+  orc::NormalStream<double> sd{seed, gidx};
   for (int64_t s = 0; s < count; ++s) {
-    if (dtype == 0) orc::normalsN<float>(seed, (uint64_t)(step0 + s), gidx, nw, (float*)out + nw * s);
-    else orc::normalsN<double>(seed, (uint64_t)(step0 + s), gidx, nw, (double*)out + nw * s);
+    if (dtype == 0) orc::normalsN<float>(sf, (uint64_t)(step0 + s), nw, (float*)out + nw * s);
+    else orc::normalsN<double>(sd, (uint64_t)(step0 + s), nw, (double*)out + nw * s);
   }
 }
 

@@ -296,10 +296,13 @@ def stats_merge(gathered: torch.Tensor, stream=None) -> torch.Tensor:
 
 def sde_noise(N: int, nsteps: int, *, seed: int, dtype=torch.float32, step0: int = 0, index_offset: int = 0,
               chunk_len: int = 0, chunk_stride: int = 0, nw: int = 3, device=None, stream=None):
-    """ens_sde_noise: (Philox words [nsteps, 4·calls, N] uint32-as-int32, normals [nsteps, nw, N])."""
+    """ens_sde_noise: (Philox words [ncalls, 4, N] uint32-as-int32 of the stream's calls
+    c0 = nw·step0 // PER …, normals [nsteps, nw, N]); PER = 4 (fp32) or 2 (fp64)."""
     dev = torch.device(device or "cuda")
-    calls = (nw + 3) // 4 if dtype == torch.float32 else (nw + 1) // 2
-    words = torch.empty((nsteps, 4 * calls, N), dtype=torch.int32, device=dev)
+    per = 4 if dtype == torch.float32 else 2
+    c0 = nw * step0 // per
+    ncalls = -(-(nw * (step0 + nsteps)) // per) - c0
+    words = torch.empty((ncalls, 4, N), dtype=torch.int32, device=dev)
     z = torch.empty((nsteps, nw, N), dtype=dtype, device=dev)
     opt = _options(0, 0, 0, 0, 0, None, 0, 0, 0, index_offset, chunk_len, chunk_stride)
     with torch.cuda.device(dev):

@@ -206,14 +206,16 @@ def test_philox_words_bitexact():
     for dt, npd in [(torch.float32, np.float32), (torch.float64, np.float64)]:
         words, z = ens.sde_noise(N, S, seed=0xDEADBEEF12345, dtype=dt, step0=17, index_offset=1 << 33)
         words = words.cpu().numpy().view(np.uint32); z = z.cpu().numpy()
-        calls = 1 if dt == torch.float32 else 2
+        per = 4 if dt == torch.float32 else 2
+        c0 = 3 * 17 // per                          # the stream's calls covering steps 17..21 (R8)
+        assert words.shape[0] == -(-(3 * (17 + S)) // per) - c0
         for i in [0, 1, 33, 69]:
             g = (1 << 33) + i
-            for s in range(S):
-                for c in range(calls):
-                    ref = oracle.philox([17 + s, g & 0xFFFFFFFF, g >> 32, c],
-                                        [0xDEADBEEF12345 & 0xFFFFFFFF, 0xDEADBEEF12345 >> 32])
-                    np.testing.assert_array_equal(words[s, 4 * c:4 * c + 4, i], ref)
+            for c in range(words.shape[0]):
+                cc = c0 + c
+                ref = oracle.philox([cc & 0xFFFFFFFF, g & 0xFFFFFFFF, g >> 32, cc >> 32],
+                                    [0xDEADBEEF12345 & 0xFFFFFFFF, 0xDEADBEEF12345 >> 32])
+                np.testing.assert_array_equal(words[c, :, i], ref)
             zr = oracle.normals(0xDEADBEEF12345, g, 17, S, "f32" if dt == torch.float32 else "f64")
             np.testing.assert_array_equal(z[:, :, i], zr.astype(npd))
 
