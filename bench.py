@@ -299,6 +299,32 @@ def main():
                 torch.cuda.get_device_properties(dev).multi_processor_count *
                 (FP32_LANES_PER_SM if tdt == torch.float32 else FP64_LANES_PER_SM) * 2 * SM_MAX_MHZ * 1e6)}
         del sol_a
+        # NEXT-1: the same ρ sweep in fp64 at the north_star's tight tolerance, Tsit5 vs Vern9
+        n_t = min(N, 10**6)
+        u0t, pt = ens.generate_inputs("lorenz", "rho_sweep", n_t, dtype=torch.float64, N_total=n_t, device=dev)
+        for alg in ["tsit5", "vern9"]:
+            sol_t = ens.solve("lorenz", alg, u0t, pt, tspan, dt, adaptive=True, abstol=1e-10, reltol=1e-10,
+                              stream=stream)
+            mst = best_ms(lambda: ens.solve("lorenz", alg, u0t, pt, tspan, dt, adaptive=True, abstol=1e-10,
+                                            reltol=1e-10, out=sol_t, stream=stream))
+            att = int((sol_t.n_accept.to(torch.int64) + sol_t.n_reject.to(torch.int64)).sum().item())
+            also[f"{alg}_f64_tol1e-10_N{n_t}"] = {"trajectories_per_s": n_t / (mst / 1e3), "kernel_ms": mst,
+                                                  "attempted_steps_per_traj": att / n_t}
+        del u0t, pt, sol_t
+        # NEXT-2: C3 (Robertson fp64, tol 1e-8, 100 save points) on Rosenbrock23 vs Rodas5
+        n_s = min(N, 10**6)
+        ur, pr = ens.generate_inputs("robertson", "random10", n_s, dtype=torch.float64, seed=0xC3, device=dev)
+        sa = [1e5 * j / 99 for j in range(100)]
+        for alg in ["rosenbrock23", "rodas5"]:
+            sol_s = ens.solve("robertson", alg, ur, pr, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8, reltol=1e-8,
+                              saveat=sa, stream=stream)
+            mss = best_ms(lambda: ens.solve("robertson", alg, ur, pr, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
+                                            reltol=1e-8, saveat=sa, out=sol_s, stream=stream))
+            att = int((sol_s.n_accept.to(torch.int64) + sol_s.n_reject.to(torch.int64)).sum().item())
+            also[f"c3_{alg}_N{n_s}"] = {"trajectories_per_s": n_s / (mss / 1e3), "kernel_ms": mss,
+                                        "attempted_steps_per_traj": att / n_s}
+            del sol_s
+        del ur, pr
 
     # end to end through the C ABI on host buffers (pinned), copies in the timed region
     e2e = None
