@@ -1,6 +1,7 @@
 """Build the sm_100a shared library libens.so in-tree (nvcc cross-compiles
 without a GPU). Flags: --fmad=false (only the explicit fmas of DESIGN §4 are
-fused), no fast-math (IEEE div/sqrt, no FTZ), -lineinfo for ncu source views.
+fused; the host side likewise with -ffp-contract=off), no fast-math (IEEE
+div/sqrt, no FTZ), -lineinfo for ncu source views.
 
 One translation unit per algorithm (csrc/k_*.cu) plus the ABI (csrc/api.cu),
 compiled in parallel into csrc/../_obj/*.o (each rebuilt only when a file it
@@ -22,7 +23,8 @@ UNITS = sorted(CSRC.glob("*.cu"))
 SRCS = UNITS + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ens.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC"]
+NVCC_FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-ffp-contract=off"]
 
 
 def nvcc() -> str:
@@ -62,6 +64,10 @@ def _compile(unit: Path, verbose: bool) -> None:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
+    stamp = OBJ / "flags.txt"
+    flags = " ".join([nvcc(), *NVCC_FLAGS])
+    if not stamp.exists() or stamp.read_text() != flags:   # compiler or flags changed: rebuild everything
+        force = True
     todo = [u for u in UNITS if force or _stale(u)]
     objs = [OBJ / (u.stem + ".o") for u in UNITS]
     if not todo and LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
@@ -72,6 +78,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
     os.replace(tmp, LIB)
+    stamp.write_text(flags)
     return LIB
 
 

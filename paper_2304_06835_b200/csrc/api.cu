@@ -176,6 +176,30 @@ bool em_save_steps(double t0, double tf, double dt, const double* sa, int k, std
   return true;
 }
 
+// Save codes of a fixed-step Tsit5 run (tsit5.cuh::tsit5_save_coded): for each
+// τ_j > t0, (s << 1) | interp with s the first step whose end tn(s) =
+// (T)(t0 + s·dt) (tf for the last step) satisfies τ_j ≤ tn(s), interp = τ_j ≠
+// tn(s). Host arithmetic mirrors the kernel's (IEEE, no contraction: the host
+// side is compiled with -ffp-contract=off).
+template <class T>
+void fixed_save_codes(double t0, double tf, double dt, int64_t nsteps, const std::vector<T>& tau,
+                      std::vector<int64_t>& code) {
+  auto tn = [&](int64_t st) -> T {
+    if (st >= nsteps) return (T)tf;
+    const double prod = (double)st * dt;
+    return (T)(t0 + prod);
+  };
+  code.assign(tau.size(), 0);
+  for (size_t j = 0; j < tau.size(); ++j) {
+    if (tau[j] <= (T)t0) continue;                       // saved at init
+    int64_t st = (int64_t)std::ceil(((double)tau[j] - t0) / dt);
+    st = std::min<int64_t>(std::max<int64_t>(st, 1), nsteps);
+    while (st > 1 && tau[j] <= tn(st - 1)) --st;
+    while (st < nsteps && tau[j] > tn(st)) ++st;
+    code[j] = (st << 1) | (tau[j] == tn(st) ? 0 : 1);
+  }
+}
+
 template <class T>
 ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0, const void* p, double t0,
                       double tf, double dt, const ens_options* opt, const ens_output* out, int n,
@@ -210,6 +234,12 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
       if (grid_saves(alg, opt)) {
         std::vector<int64_t> st;
         if (!em_save_steps(t0, tf, dt, opt->saveat, a.k, st)) return ENS_E_BAD_SAVEAT;
+        if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
+          return ENS_E_CUDA;
+      } else if (alg == ENS_TSIT5 && !opt->adaptive) {
+        std::vector<int64_t> st;
+        fixed_save_codes<T>(t0, tf, dt, nsteps, tau, st);
+        a.save_grid_only = std::all_of(st.begin(), st.end(), [](int64_t c) { return (c & 1) == 0; });
         if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return ENS_E_CUDA;
       }

@@ -15,14 +15,25 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       // fp32: two trajectories per thread on the packed FFMA2 path
       const auto cf = make_tsit_coef<float, float2>(a.dt0, a.h_last);
       const int64_t threads = cdiv(a.N, 2);
-      const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
-      if (save) tsit5_fixed_kernel<M, f2, true><<<g2, b2, 0, s>>>(a, cf);
-      else tsit5_fixed_kernel<M, f2, false><<<g2, b2, 0, s>>>(a, cf);
+      if (save) {
+        // the saving instances hold more registers: pick the block size with the most resident warps
+        auto kern = a.save_grid_only ? tsit5_fixed_kernel<M, f2, 2> : tsit5_fixed_kernel<M, f2, 1>;
+        const dim3 b2(occupancy_block(kern, threads));
+        kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, 0, s>>>(a, cf);
+      } else {
+        const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
+        tsit5_fixed_kernel<M, f2, 0><<<g2, b2, 0, s>>>(a, cf);
+      }
     } else {
       const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
-      const dim3 g = grid_for(a.N), b(solver_block(a.N));
-      if (save) tsit5_fixed_kernel<M, double, true><<<g, b, 0, s>>>(a, cf);
-      else tsit5_fixed_kernel<M, double, false><<<g, b, 0, s>>>(a, cf);
+      if (save) {
+        auto kern = a.save_grid_only ? tsit5_fixed_kernel<M, double, 2> : tsit5_fixed_kernel<M, double, 1>;
+        const dim3 b(occupancy_block(kern, a.N));
+        kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a, cf);
+      } else {
+        const dim3 g = grid_for(a.N), b(solver_block(a.N));
+        tsit5_fixed_kernel<M, double, 0><<<g, b, 0, s>>>(a, cf);
+      }
     }
   } else {
     // (a two-trajectories-per-thread f2 variant of the adaptive step measured 4 % slower:

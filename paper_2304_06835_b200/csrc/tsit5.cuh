@@ -154,6 +154,16 @@ __device__ __forceinline__ void load_lanes(const Args<T>& a, const int64_t (&idx
 template <int n, class V, class T>
 __device__ __forceinline__ void store_lanes(const Args<T>& a, const int64_t (&idx)[LaneOf<V>::W],
                                             const bool (&live)[LaneOf<V>::W], int j, const V (&v)[n]) {
+  if constexpr (LaneOf<V>::W == 2) {
+    // a thread's two trajectories are neighbours in memory: one 8-byte store per
+    // component (a warp writes 256 contiguous bytes) when the pair is 8-byte aligned
+    if (live[1] && (a.ld % 2) == 0 && (reinterpret_cast<uintptr_t>(a.u_out) & 7) == 0) {
+#pragma unroll
+      for (int c = 0; c < n; ++c)
+        *reinterpret_cast<float2*>(a.u_out + ((size_t)j * n + c) * a.ld + idx[0]) = v[c].v;
+      return;
+    }
+  }
 #pragma unroll
   for (int w = 0; w < LaneOf<V>::W; ++w)
     if (live[w]) {
@@ -190,11 +200,43 @@ __device__ __forceinline__ void tsit5_save(const Args<T>& a, const int64_t (&idx
   }
 }
 
+// Fixed-step saves by precomputed step codes (host: fixed_save_codes in api.cu):
+// save_step[j] = (s << 1) | interp, s = the 1-based step after which τ_j is
+// stored — the first s with τ_j ≤ tn(s), tn(s) = (T)(t0 + s·dt) (tf for the
+// last step), the same comparison the per-step scan made — and interp = 0 if
+// τ_j == tn(s) exactly (store u_{s}) else 1 (interpolant at θ = (τ_j − t)/h).
+// Steps without a save then cost one integer compare instead of a time
+// computation and a τ load.
+template <int n, class V, class T, bool INTERP>
+__device__ __forceinline__ void tsit5_save_coded(const Args<T>& a, const int64_t (&idx)[LaneOf<V>::W],
+                                                 const bool (&live)[LaneOf<V>::W], int& js, int64_t& next,
+                                                 int64_t s, T h, const V (&u)[n], const V (&K)[7][n],
+                                                 const V (&un)[n]) {
+  while (js < a.k) {
+    const int64_t code = __ldg(a.save_step + js);
+    if ((code >> 1) != s + 1) { next = code >> 1; return; }
+    if (INTERP && (code & 1)) {
+      const T t = (T)(a.t0d + (double)s * a.dtd);
+      V o[n];
+      tsit5_interp<n, V>(splat<V>((__ldg(a.tau + js) - t) / h), splat<V>(h), u, K, o);
+      store_lanes<n, V, T>(a, idx, live, js, o);
+    } else {
+      store_lanes<n, V, T>(a, idx, live, js, un);
+    }
+    ++js;
+  }
+  next = -1;
+}
+
 // ---------------------------------------------------------------- fixed dt --
 // Fixed grid (DESIGN R3): nsteps steps of dt, the last of h_last. No error
 // estimate. Divergence is checked on f(u0) and the final state (DESIGN R6).
 // V = float2-pair (two trajectories per thread), float or double.
-template <class M, class V, bool SAVE>
+// SAVE: 0 = final state only; 1 = saveat with interpolation between grid
+// points; 2 = every save point on the step grid (no interpolant, so the stage
+// vectors are dead after each step: fewer registers, coefficients stay in
+// uniform registers).
+template <class M, class V, int SAVE>
 __global__ void __launch_bounds__(256)
     tsit5_fixed_kernel(const Args<typename LaneOf<V>::T> a, const TsitCoef<typename CoefOf<V>::C> cf) {
   using T = typename LaneOf<V>::T;
@@ -234,20 +276,21 @@ __global__ void __launch_bounds__(256)
   if (!any) return;
   const V hdt = splat<V>(a.dt0);
   const HaParam<V, C> ha{cf.h};
-  // all steps but the last: constant h (no per-step select in the hot loop)
+  int64_t next = -1;   // step after which the next save falls (SAVE)
+  if (SAVE && js < a.k) next = __ldg(a.save_step + js) >> 1;
+  // all steps but the last: constant h (no per-step select in the hot loop).
+  // Stage times are not needed: the models are autonomous (time argument ignored).
   for (int64_t s = 0; s + 1 < steps; ++s) {
-    T t = T(0);
-    if (SAVE) t = (T)(a.t0d + (double)s * a.dtd);
-    tsit5_stages<M, V>(par, splat<V>(t), hdt, ha, u, K, y);
-    if (SAVE) tsit5_save<n, V, T>(a, idx, live, js, t, (T)(a.t0d + (double)(s + 1) * a.dtd), a.dt0, u, K, y);
+    tsit5_stages<M, V>(par, splat<V>(T(0)), hdt, ha, u, K, y);
+    if (SAVE && next == s + 1) tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, s, a.dt0, u, K, y);
 #pragma unroll
     for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
   }
   {   // last step: h_last, lands on tf exactly
-    const T t = (T)(a.t0d + (double)(steps - 1) * a.dtd);
     const HaParam<V, C> hal{cf.hl};
-    tsit5_stages<M, V>(par, splat<V>(t), splat<V>(a.h_last), hal, u, K, y);
-    if (SAVE) tsit5_save<n, V, T>(a, idx, live, js, t, a.tf, a.h_last, u, K, y);
+    tsit5_stages<M, V>(par, splat<V>(T(0)), splat<V>(a.h_last), hal, u, K, y);
+    if (SAVE && next == steps)
+      tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, steps - 1, a.h_last, u, K, y);
   }
   if (SAVE) {
     V nanv[n];

@@ -114,6 +114,13 @@ def main():
             run("C2-adaptive", "lorenz", "tsit5", "rho_sweep", N, "f32", (0.0, 1.0), 1e-3, "tsit5_adaptive",
                 adaptive=True, abstol=1e-6, reltol=1e-6, refill=refill)
     run("C2-fixed", "lorenz", "tsit5", "rho_sweep", big, "f64", (0.0, 1.0), 1e-3, "tsit5_fixed")
+    # saveat-dense: every one of the 1001 grid points stored, [1001][3][N] fp32 — the HBM-write
+    # side of the roofline (12 B per trajectory-step against 192 FLOP)
+    sa_all = [j * 1e-3 for j in range(1001)]
+    sa_all[-1] = 1.0
+    for Nd in [10**6, 4 * 10**6]:
+        run("C2-saveat-dense", "lorenz", "tsit5", "rho_sweep", Nd, "f32", (0.0, 1.0), 1e-3, "tsit5_fixed", reps=3,
+            saveat=sa_all)
     # the C2 adaptive ensemble with its columns randomly permuted: neighbouring lanes no longer have
     # similar step counts (20-47), the divergence the refill scheduler (a8) is for
     for refill in [False, True]:

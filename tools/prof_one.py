@@ -26,6 +26,12 @@ elif name in ("c2a_refill", "c2a_shuf", "c2a_shuf_refill"):
     rf = name.endswith("refill")
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6,
                           refill=rf)
+elif name == "dense":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float32, N_total=N)
+    sa = [j * 1e-3 for j in range(1001)]
+    sa[-1] = 1.0
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, saveat=sa)
 elif name == "c1":
     N = N or 1024
     u0, p = ens.generate_inputs("lorenz", "random10", N, dtype=torch.float64, seed=0xC1)
