@@ -7,6 +7,17 @@
 
 namespace ens {
 
+// Bulk save rows must start on 16-byte boundaries: u_out aligned and ld·sizeof(T)
+// a multiple of 16 (block starts are multiples of 128 B). ENS_TUNE_BULK_SAVES=0 disables.
+template <class T>
+bool bulk_saves_ok(const Args<T>& a) {
+  static const bool enabled = [] {
+    const char* e = getenv("ENS_TUNE_BULK_SAVES");
+    return !(e && atoi(e) == 0);
+  }();
+  return enabled && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 && ((size_t)a.ld * sizeof(T)) % 16 == 0;
+}
+
 template <class M, class T>
 ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
@@ -17,9 +28,11 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       const int64_t threads = cdiv(a.N, 2);
       if (save) {
         // the saving instances hold more registers: pick the block size with the most resident warps
-        auto kern = a.save_grid_only ? tsit5_fixed_kernel<M, f2, 2> : tsit5_fixed_kernel<M, f2, 1>;
+        auto kern = !a.save_grid_only ? tsit5_fixed_kernel<M, f2, 1>
+                    : bulk_saves_ok(a) ? tsit5_fixed_kernel<M, f2, 3> : tsit5_fixed_kernel<M, f2, 2>;
         const dim3 b2(occupancy_block(kern, threads));
-        kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, 0, s>>>(a, cf);
+        const size_t smem = (a.save_grid_only && bulk_saves_ok(a)) ? 2 * M::n * b2.x * 2 * sizeof(float) : 0;
+        kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, smem, s>>>(a, cf);
       } else {
         const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
         tsit5_fixed_kernel<M, f2, 0><<<g2, b2, 0, s>>>(a, cf);
@@ -27,9 +40,11 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
     } else {
       const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
       if (save) {
-        auto kern = a.save_grid_only ? tsit5_fixed_kernel<M, double, 2> : tsit5_fixed_kernel<M, double, 1>;
+        auto kern = !a.save_grid_only ? tsit5_fixed_kernel<M, double, 1>
+                    : bulk_saves_ok(a) ? tsit5_fixed_kernel<M, double, 3> : tsit5_fixed_kernel<M, double, 2>;
         const dim3 b(occupancy_block(kern, a.N));
-        kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a, cf);
+        const size_t smem = (a.save_grid_only && bulk_saves_ok(a)) ? 2 * M::n * b.x * sizeof(double) : 0;
+        kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, smem, s>>>(a, cf);
       } else {
         const dim3 g = grid_for(a.N), b(solver_block(a.N));
         tsit5_fixed_kernel<M, double, 0><<<g, b, 0, s>>>(a, cf);

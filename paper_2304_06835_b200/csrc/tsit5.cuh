@@ -228,6 +228,57 @@ __device__ __forceinline__ void tsit5_save_coded(const Args<T>& a, const int64_t
   next = -1;
 }
 
+// Bulk (TMA-engine) stores of grid saves: every thread of a full block puts its
+// values into a shared-memory row buffer; one thread then streams each
+// component row — blockDim·W contiguous values — to global memory with
+// cp.async.bulk (UBLKCP), double-buffered, so the save traffic leaves the SM as
+// large asynchronous writes instead of per-thread stores in the step loop.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int n, class V, class T>
+__device__ __forceinline__ void tsit5_save_bulk(const Args<T>& a, const bool (&live)[LaneOf<V>::W], int& js,
+                                                int& nb, int64_t& next, int64_t s, const V (&un)[n], int64_t blk0,
+                                                T* smem) {
+  constexpr int W = LaneOf<V>::W;
+  const int BW = blockDim.x * W;
+  while (js < a.k) {
+    const int64_t code = __ldg(a.save_step + js);
+    if ((code >> 1) != s + 1) { next = code >> 1; return; }
+    T* buf = smem + (size_t)(nb & 1) * n * BW;
+    if (nb >= 2) {                            // this buffer was last read by the copies of save nb − 2
+      if (threadIdx.x == 0) bulk_wait_read1();
+      __syncthreads();
+    }
+#pragma unroll
+    for (int c = 0; c < n; ++c) {
+      if constexpr (W == 2) {
+        *reinterpret_cast<float2*>(buf + (size_t)c * BW + 2 * threadIdx.x) =
+            make_float2(live[0] ? lane(un[c], 0) : nanT<float>(), live[1] ? lane(un[c], 1) : nanT<float>());
+      } else {
+        buf[(size_t)c * BW + threadIdx.x] = live[0] ? lane(un[c], 0) : nanT<T>();
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c < n; ++c)
+        bulk_s2g(a.u_out + ((size_t)js * n + c) * a.ld + blk0, buf + (size_t)c * BW, (uint32_t)(BW * sizeof(T)));
+      bulk_commit();
+    }
+    ++nb;
+    ++js;
+  }
+  next = -1;
+}
+
 // ---------------------------------------------------------------- fixed dt --
 // Fixed grid (DESIGN R3): nsteps steps of dt, the last of h_last. No error
 // estimate. Divergence is checked on f(u0) and the final state (DESIGN R6).
@@ -235,13 +286,19 @@ __device__ __forceinline__ void tsit5_save_coded(const Args<T>& a, const int64_t
 // SAVE: 0 = final state only; 1 = saveat with interpolation between grid
 // points; 2 = every save point on the step grid (no interpolant, so the stage
 // vectors are dead after each step: fewer registers, coefficients stay in
-// uniform registers).
+// uniform registers); 3 = as 2, full blocks stream their saves through shared
+// memory with bulk copies (dynamic shared memory 2·n·blockDim·W·sizeof(T);
+// the host checks the 16-byte alignment of every row).
 template <class M, class V, int SAVE>
 __global__ void __launch_bounds__(256)
     tsit5_fixed_kernel(const Args<typename LaneOf<V>::T> a, const TsitCoef<typename CoefOf<V>::C> cf) {
   using T = typename LaneOf<V>::T;
   using C = typename CoefOf<V>::C;
   constexpr int n = M::n, W = LaneOf<V>::W;
+  extern __shared__ __align__(16) unsigned char ens_fixed_smem[];
+  const int64_t blk0 = (int64_t)blockIdx.x * blockDim.x * W;
+  // bulk saves need every thread of the block at every barrier: full blocks only
+  const bool bulk = (SAVE == 3) && (blk0 + (int64_t)blockDim.x * W <= a.N);
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
   if (i0 >= a.N) return;
   int64_t idx[W];
@@ -273,7 +330,8 @@ __global__ void __launch_bounds__(256)
   bool any = false;
 #pragma unroll
   for (int w = 0; w < W; ++w) any = any || live[w];
-  if (!any) return;
+  if (!any && !bulk) return;    // (in a bulk block a finished thread stays for the barriers, saving NaN)
+  int nb = 0;                   // bulk saves issued by this block
   const V hdt = splat<V>(a.dt0);
   const HaParam<V, C> ha{cf.h};
   int64_t next = -1;   // step after which the next save falls (SAVE)
@@ -282,16 +340,26 @@ __global__ void __launch_bounds__(256)
   // Stage times are not needed: the models are autonomous (time argument ignored).
   for (int64_t s = 0; s + 1 < steps; ++s) {
     tsit5_stages<M, V>(par, splat<V>(T(0)), hdt, ha, u, K, y);
-    if (SAVE && next == s + 1) tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, s, a.dt0, u, K, y);
+    if (SAVE && next == s + 1) {
+      if (SAVE == 3 && bulk)
+        tsit5_save_bulk<n, V, T>(a, live, js, nb, next, s, y, blk0, reinterpret_cast<T*>(ens_fixed_smem));
+      else
+        tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, s, a.dt0, u, K, y);
+    }
 #pragma unroll
     for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
   }
   {   // last step: h_last, lands on tf exactly
     const HaParam<V, C> hal{cf.hl};
     tsit5_stages<M, V>(par, splat<V>(T(0)), splat<V>(a.h_last), hal, u, K, y);
-    if (SAVE && next == steps)
-      tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, steps - 1, a.h_last, u, K, y);
+    if (SAVE && next == steps) {
+      if (SAVE == 3 && bulk)
+        tsit5_save_bulk<n, V, T>(a, live, js, nb, next, steps - 1, y, blk0, reinterpret_cast<T*>(ens_fixed_smem));
+      else
+        tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, steps - 1, a.h_last, u, K, y);
+    }
   }
+  if (SAVE == 3 && bulk && threadIdx.x == 0) bulk_wait_all();
   if (SAVE) {
     V nanv[n];
 #pragma unroll
