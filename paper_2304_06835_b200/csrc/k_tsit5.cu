@@ -8,12 +8,15 @@
 namespace ens {
 
 // Bulk save rows must start on 16-byte boundaries: u_out aligned and ld·sizeof(T)
-// a multiple of 16 (block starts are multiples of 128 B). ENS_TUNE_BULK_SAVES=0 disables.
+// a multiple of 16 (block starts are multiples of 128 B). Off by default: on the
+// saveat-dense config the two block barriers per save cost more than the per-thread
+// 8-byte stores they replace (15.9 vs 15.2 ms, profiles/bulk_saves_vs_stg_r01.jsonl);
+// ENS_TUNE_BULK_SAVES=1 enables (tests/test_gpu_saves.py runs it in a subprocess).
 template <class T>
 bool bulk_saves_ok(const Args<T>& a) {
   static const bool enabled = [] {
     const char* e = getenv("ENS_TUNE_BULK_SAVES");
-    return !(e && atoi(e) == 0);
+    return e && atoi(e) == 1;
   }();
   return enabled && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 && ((size_t)a.ld * sizeof(T)) % 16 == 0;
 }
