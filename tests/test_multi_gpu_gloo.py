@@ -1,4 +1,4 @@
-"""Host-side multi-rank logic on CPU with gloo, world_size 2 (-m "not gpu").
+"""Host-side multi-rank logic on CPU with gloo, world_size 2 and 4 (-m "not gpu").
 
 Covers the sharding maps (every global trajectory exactly once, inputs of a
 shard = the slice of the global inputs), and the two exchange steps of
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q):
         else:
             assert out is None
         # each rank's shard inputs equal the slice of the global ensemble
-        N_total = 2 * 4096
+        N_total = world * 4096
         for sh in [mg.shard_contiguous(N_total, rank, world), mg.shard_block_cyclic(N_total, rank, world, chunk=512)]:
             u0, p = make_inputs("lorenz", "random10", sh.n_local, seed=0xC5, index_offset=sh.index_offset,
                                 chunk_len=sh.chunk_len, chunk_stride=sh.chunk_stride)
@@ -60,17 +60,18 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_exchange_gloo():
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_exchange_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    res = dict(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
 
 
 @pytest.mark.parametrize("N,R", [(10**8, 8), (10**7 + 3, 4), (5, 2), (1 << 20, 8)])
