@@ -120,6 +120,10 @@ typedef struct {
   int64_t index_offset;    /* global index of local trajectory 0 (Philox counter; multi-GPU shard) */
   int64_t chunk_len, chunk_stride; /* 0,0: contiguous. Else global(i) = index_offset +
                               (i / chunk_len) * chunk_stride + i % chunk_len (block-cyclic shard) */
+  int64_t out_ld;          /* ensemble_solve: leading dimension (elements) of the u_out rows, >= N;
+                              0 -> N. Lets a shard write its states straight into a slice of a larger
+                              [k][n][out_ld] array — e.g. another GPU's gather buffer mapped through CUDA
+                              IPC (the fused gather of multi_gpu.PeerGather). ensemble_solve_host: must be 0. */
 } ens_options;
 
 typedef struct {

@@ -39,7 +39,7 @@ class _Options(ctypes.Structure):
                 ("max_steps", ctypes.c_int64), ("seed", ctypes.c_uint64), ("saveat", ctypes.c_void_p),
                 ("n_saveat", ctypes.c_int32), ("p_broadcast", ctypes.c_int32), ("want_stats", ctypes.c_int32),
                 ("refill", ctypes.c_int32), ("index_offset", ctypes.c_int64), ("chunk_len", ctypes.c_int64),
-                ("chunk_stride", ctypes.c_int64)]
+                ("chunk_stride", ctypes.c_int64), ("out_ld", ctypes.c_int64)]
 
 
 class _Output(ctypes.Structure):
@@ -186,6 +186,16 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
                        n_accept=torch.empty(N, dtype=torch.int32, device=dev),
                        n_reject=torch.empty(N, dtype=torch.int32, device=dev),
                        stats=torch.empty((max(k, 1), n, 3), dtype=torch.float64, device=dev) if stats else None)
+    if out.u is not None:
+        # u_out may be a column slice of a larger [k][n][L] / [n][L] array (e.g. a peer GPU's gather
+        # buffer): rows of L elements, trajectory-contiguous
+        u = out.u
+        if u.dtype != u0.dtype or u.shape[-1] != N or u.stride(-1) != 1:
+            raise ValueError("out.u must have the input dtype, N trajectories in its last dimension, stride 1")
+        ld_rows = u.stride(-2)
+        if u.dim() == 3 and u.stride(0) != u.shape[1] * ld_rows:
+            raise ValueError("out.u: save points must be stacked with the row stride")
+        opt.out_ld = 0 if ld_rows == N else int(ld_rows)
     L = lib()
     wsb = L.ens_workspace_bytes(MODELS[model], ALGS[alg], DTYPES[u0.dtype], N, ctypes.byref(opt))
     if workspace is None:

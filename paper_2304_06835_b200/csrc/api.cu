@@ -130,6 +130,7 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
   if (alg < ENS_TSIT5 || alg > ENS_VERN9 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
+  if (opt->out_ld != 0 && opt->out_ld < N) return ENS_E_INVALID_ARG;
   const bool sde = nw > 0;
   if (sde != is_sde_alg(alg)) return ENS_E_ALG_MISMATCH;
   // events (DESIGN R18) are located on the adaptive Tsit5 interpolant only
@@ -207,7 +208,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   const Layout L = layout(n, alg, sizeof(T) == 4 ? ENS_F32 : ENS_F64, N, opt);
   char* ws = (char*)out->workspace;
   Args<T> a{};
-  a.N = N; a.ld = ld;
+  a.N = N; a.ld = ld; a.ldo = opt->out_ld > 0 ? opt->out_ld : ld;
   a.u0 = (const T*)u0; a.p = (const T*)p; a.p_broadcast = opt->p_broadcast;
   a.t0d = t0; a.tfd = tf; a.dtd = dt;
   a.t0 = (T)t0; a.tf = (T)tf;
@@ -253,7 +254,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   if (opt->want_stats) {
     if (!is_sde_alg(alg)) {
       const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
-      stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, kStatsChunk, a.partial);
+      stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, a.ldo, kStatsChunk, a.partial);
     }
     const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for(N).x : L.nparts;
     stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
@@ -308,7 +309,7 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   int n = 0, m = 0, nw = 0;
   ens_status st = validate(model, alg, dtype, N, t0, tf, dt, opt, &n);
   if (st != ENS_OK) return st;
-  if (opt->want_stats) return ENS_E_UNSUPPORTED;
+  if (opt->want_stats || opt->out_ld != 0) return ENS_E_UNSUPPORTED;
   if (!u0_host || !p_host || !d_u0 || !d_p || !d_u_out || !u_out_host) return ENS_E_INVALID_ARG;
   const int64_t C = std::max<int64_t>(1, std::min<int64_t>(n_chunks, N));
   // Philox counters key on the global trajectory index (DESIGN R10): each chunk
@@ -452,8 +453,8 @@ ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int32_t
   const int64_t nparts = cdiv(N, kStatsChunk);
   const dim3 g((unsigned)nparts, (unsigned)rows);
   double* part = (double*)workspace;
-  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, kStatsChunk, part);
-  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, kStatsChunk, part);
+  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, N, kStatsChunk, part);
+  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, N, kStatsChunk, part);
   stats_merge_kernel<<<rows, 256, 0, s>>>(part, (int)nparts, stats);
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }

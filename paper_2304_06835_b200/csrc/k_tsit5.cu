@@ -18,7 +18,7 @@ bool bulk_saves_ok(const Args<T>& a) {
     const char* e = getenv("ENS_TUNE_BULK_SAVES");
     return e && atoi(e) == 1;
   }();
-  return enabled && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 && ((size_t)a.ld * sizeof(T)) % 16 == 0;
+  return enabled && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 && ((size_t)a.ldo * sizeof(T)) % 16 == 0;
 }
 
 template <class M, class T>

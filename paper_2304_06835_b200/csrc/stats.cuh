@@ -61,12 +61,12 @@ __device__ __forceinline__ Moments chan_merge(Moments a, Moments b) {
 // Partials over a stored [rows][N] array in T: grid (nparts, rows); block b
 // reduces elements [b*chunk, (b+1)*chunk) of its row.
 template <class T>
-__global__ void __launch_bounds__(256) stats_partial_kernel(const T* __restrict__ x, int64_t N, int64_t chunk,
-                                                            double* __restrict__ partial) {
+__global__ void __launch_bounds__(256) stats_partial_kernel(const T* __restrict__ x, int64_t N, int64_t ld,
+                                                            int64_t chunk, double* __restrict__ partial) {
   __shared__ double red[32];
   const int row = blockIdx.y;
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(N, lo + chunk);
-  const T* xr = x + (size_t)row * N;
+  const T* xr = x + (size_t)row * ld;
   double c = 0, s = 0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const double v = (double)xr[i];

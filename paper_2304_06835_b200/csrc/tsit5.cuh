@@ -157,10 +157,10 @@ __device__ __forceinline__ void store_lanes(const Args<T>& a, const int64_t (&id
   if constexpr (LaneOf<V>::W == 2) {
     // a thread's two trajectories are neighbours in memory: one 8-byte store per
     // component (a warp writes 256 contiguous bytes) when the pair is 8-byte aligned
-    if (live[1] && (a.ld % 2) == 0 && (reinterpret_cast<uintptr_t>(a.u_out) & 7) == 0) {
+    if (live[1] && (a.ldo % 2) == 0 && (reinterpret_cast<uintptr_t>(a.u_out) & 7) == 0) {
 #pragma unroll
       for (int c = 0; c < n; ++c)
-        *reinterpret_cast<float2*>(a.u_out + ((size_t)j * n + c) * a.ld + idx[0]) = v[c].v;
+        *reinterpret_cast<float2*>(a.u_out + ((size_t)j * n + c) * a.ldo + idx[0]) = v[c].v;
       return;
     }
   }
@@ -168,7 +168,7 @@ __device__ __forceinline__ void store_lanes(const Args<T>& a, const int64_t (&id
   for (int w = 0; w < LaneOf<V>::W; ++w)
     if (live[w]) {
 #pragma unroll
-      for (int c = 0; c < n; ++c) a.u_out[((size_t)j * n + c) * a.ld + idx[w]] = lane(v[c], w);
+      for (int c = 0; c < n; ++c) a.u_out[((size_t)j * n + c) * a.ldo + idx[w]] = lane(v[c], w);
     }
 }
 
@@ -270,7 +270,7 @@ __device__ __forceinline__ void tsit5_save_bulk(const Args<T>& a, const bool (&l
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int c = 0; c < n; ++c)
-        bulk_s2g(a.u_out + ((size_t)js * n + c) * a.ld + blk0, buf + (size_t)c * BW, (uint32_t)(BW * sizeof(T)));
+        bulk_s2g(a.u_out + ((size_t)js * n + c) * a.ldo + blk0, buf + (size_t)c * BW, (uint32_t)(BW * sizeof(T)));
       bulk_commit();
     }
     ++nb;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256)
       for (int j = js; j < (SAVE ? a.k : 1); ++j)
 #pragma unroll
         for (int c = 0; c < n; ++c)
-          a.u_out[((size_t)j * n + c) * a.ld + idx[w]] = SAVE ? nanT<T>() : lane(u[c], w);
+          a.u_out[((size_t)j * n + c) * a.ldo + idx[w]] = SAVE ? nanT<T>() : lane(u[c], w);
       if (a.retcode) a.retcode[idx[w]] = RET_DIVERGED;
       if (a.nacc) a.nacc[idx[w]] = 0;
       if (a.nrej) a.nrej[idx[w]] = 0;

@@ -8,7 +8,9 @@ is bit-identical for any world size). The two real exchange steps come after
 the solve:
   1. ensemble statistics: all-gather of each rank's (count, mean, M2) triples,
      then a fixed rank-order Chan merge on every rank (deterministic);
-  2. optional gather of final / saved states to rank 0.
+  2. optional gather of final / saved states to rank 0 — either an NCCL
+     gather after the solve, or fused into it (PeerGather: the solver stores
+     into rank 0's array through CUDA IPC / NVLink while it runs).
 Collectives go through torch.distributed (NCCL on GPUs; the same code runs on
 gloo with CPU tensors for the host-side tests).
 """
@@ -79,6 +81,53 @@ def merge_stats(gathered: torch.Tensor) -> torch.Tensor:
     if not gathered.is_cuda:
         raise RuntimeError("merge_stats runs on the GPU (no CPU path)")
     return ens.stats_merge(gathered)
+
+
+class PeerGather:
+    """Gather fused into the solve (SURVEY §8e exchange 2): rank `dst` owns the
+    global state array [*lead, N_total]; its CUDA IPC handle goes to every rank,
+    which passes its column slice [*lead, off:off+N_r] as the solver's output
+    (ens_options.out_ld = N_total). Each trajectory's final / saved states are
+    then stored by the solver kernel straight into the destination GPU's memory
+    (NVLink peer stores, P2P enabled lazily by the IPC mapping) while the solve
+    runs — no separate gather collective after it. `complete()` orders the
+    destination's later reads after every rank's solve: a one-element NCCL
+    all-reduce on the stream (device-side), or a host barrier on gloo.
+
+    Shards must be contiguous (`shard_contiguous` / `shard_weak`)."""
+
+    def __init__(self, lead: tuple, n_local: int, index_offset: int, n_total: int, dtype, device, dst: int = 0,
+                 group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.group, self.dst, self.device = group, dst, torch.device(device)
+        me = dist.get_rank(group)
+        self.buf = None
+        payload = [None]
+        if me == dst:
+            self.buf = torch.empty((*lead, n_total), dtype=dtype, device=self.device)
+            payload = [reduce_tensor(self.buf)]
+        dist.broadcast_object_list(payload, src=dst, group=group)
+        if me == dst:
+            remote = self.buf
+        else:
+            fn, args = payload[0]
+            remote = fn(*args)                      # the destination's array, mapped through CUDA IPC
+        self.view = remote[..., index_offset:index_offset + n_local]
+        self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    def out(self) -> torch.Tensor:
+        """This rank's slice of the destination array: pass as the solver output (Solution.u)."""
+        return self.view
+
+    def complete(self) -> Optional[torch.Tensor]:
+        """After the solve: every rank's stores are ordered before the destination's reads.
+        Returns the full array on `dst`, None elsewhere."""
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+        return self.buf
 
 
 def gather_states(local: torch.Tensor, dst: int = 0, group=None) -> Optional[torch.Tensor]:

@@ -94,6 +94,8 @@ def _call(model, alg, dtype=0, N=16, t0=0.0, tf=1.0, dt=1e-3, **o):
     (dict(model="ball", alg="rodas5", adaptive=1, abstol=1e-6), 8),
     (dict(model="lorenz", alg="vern9", saveat=[0.00015]), 6),
     (dict(model="pollu", alg="vern9", dtype=1), 8),                                # n = 20: stiff solvers only
+    (dict(model="lorenz", alg="tsit5", N=16, out_ld=8), 1),                        # out_ld < N
+    (dict(model="lorenz", alg="tsit5", N=16, out_ld=32), 7),                       # wider rows: valid
 ])
 def test_validation_statuses(kw, status):
     assert _call(**kw) == status
