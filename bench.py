@@ -164,7 +164,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=98304)
     ap.add_argument("--ref-sample", type=int, default=16384)
-    ap.add_argument("--no-gather", action="store_true", help="skip the NCCL gather of final states (N>1)")
+    ap.add_argument("--no-gather", action="store_true", help="skip the gather of final states (N>1)")
+    ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
+                    help="N>1 state gather: 'peer' = fused into the solve (CUDA IPC / NVLink stores into rank 0's "
+                         "array, multi_gpu.PeerGather), 'nccl' = NCCL gather after the solve")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-also", action="store_true", help="skip the fp64-fixed / adaptive side measurements")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
@@ -206,7 +209,15 @@ def main():
     # a1: inputs generated on device from (seed, global index) — no host scatter
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=tdt, index_offset=shard.index_offset,
                                 N_total=N_total, device=dev)
-    sol = ens.Solution(u=torch.empty((3, N), dtype=tdt, device=dev),
+    gather_mode = "none" if (world == 1 or args.no_gather) else args.gather
+    peer = None
+    if gather_mode == "peer":
+        try:
+            peer = mg.PeerGather((3,), N, shard.index_offset, N_total, tdt, dev)
+        except Exception as e:   # IPC mapping unavailable: gather with NCCL after the solve instead
+            print(f"PeerGather unavailable ({e!r}); using the NCCL gather", file=sys.stderr)
+            gather_mode = "nccl"
+    sol = ens.Solution(u=peer.out() if peer is not None else torch.empty((3, N), dtype=tdt, device=dev),
                        retcode=torch.empty(N, dtype=torch.int32, device=dev),
                        n_accept=torch.empty(N, dtype=torch.int32, device=dev),
                        n_reject=torch.empty(N, dtype=torch.int32, device=dev), stats=None)
@@ -224,13 +235,15 @@ def main():
         n_l += 1
         if ev_k1 is not None:
             ev_k1.record(stream)
-        ens.ensemble_stats(sol.u.view(1, 3, N), out=st_local, workspace=sws, stream=stream)
+        ens.ensemble_stats(sol.u.unsqueeze(0), out=st_local, workspace=sws, stream=stream)
         n_l += 2
         if world > 1:
             g = mg.allgather_stats(st_local)
             mg.merge_stats(g)
             n_l += 1
-            if not args.no_gather:
+            if gather_mode == "peer":
+                peer.complete()          # the states are already in rank 0's array; order its reads
+            elif gather_mode == "nccl":
                 mg.gather_states(sol.u)
         launches_per_step[0] = n_l
 
@@ -372,7 +385,7 @@ def main():
                        "N_per_gpu": N, "N_total": N_total, "tspan": [0.0, 1.0], "dt": dt, "nsteps": nsteps,
                        "parallelism": f"dp{world} (trajectory shards)", "l2": "inputs+outputs (360 MB) > L2 (126 MB)",
                        "step": "ensemble_solve + ensemble_stats" + (" + NCCL allgather(stats)+merge" +
-                                                                    ("" if args.no_gather else " + NCCL gather(states)")
+                                                                    {"none": "", "nccl": " + NCCL gather(states)", "peer": " (states stored into rank 0's array by the solve: fused peer gather)"}[gather_mode]
                                                                     if world > 1 else "")},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": load_traffic(tag),

@@ -178,10 +178,12 @@ ens_status ens_generate_inputs(ens_model model, ens_dtype dtype, ens_recipe reci
                                void* stream);
 
 /* Ensemble statistics of a stored state array (DESIGN R12): x is device
- * T [rows][N] (e.g. u_out viewed as [k·n][N]); writes (count, mean, M2) of the
- * finite values of each row to stats [rows][3] (fp64). Deterministic (fixed
- * two-level reduction order). workspace: device, >= ens_stats_workspace_bytes. */
-ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int32_t rows, double* stats,
+ * T, rows of N values whose starts are ld elements apart (ld >= N; ld = N for a
+ * dense [rows][N] array such as u_out viewed as [k·n][N], larger for a slice of
+ * a wider array); writes (count, mean, M2) of the finite values of each row to
+ * stats [rows][3] (fp64). Deterministic (fixed two-level reduction order).
+ * workspace: device, >= ens_stats_workspace_bytes. */
+ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int64_t ld, int32_t rows, double* stats,
                               void* workspace, size_t workspace_bytes, void* stream);
 size_t ens_stats_workspace_bytes(int64_t N, int32_t rows);
 

@@ -73,7 +73,7 @@ def lib() -> ctypes.CDLL:
         L.ensemble_solve_host.restype = i32
         L.ens_generate_inputs.argtypes = [i32, i32, i32, u64, i64, i64, ctypes.POINTER(_Options), vp, vp, vp]
         L.ens_generate_inputs.restype = i32
-        L.ens_ensemble_stats.argtypes = [i32, vp, i64, i32, vp, vp, sz, vp]
+        L.ens_ensemble_stats.argtypes = [i32, vp, i64, i64, i32, vp, vp, sz, vp]
         L.ens_ensemble_stats.restype = i32
         L.ens_stats_workspace_bytes.argtypes = [i64, i32]
         L.ens_stats_workspace_bytes.restype = sz
@@ -266,7 +266,12 @@ def ensemble_stats(x: torch.Tensor, *, out: Optional[torch.Tensor] = None, works
     """ens_ensemble_stats: (count, mean, M2) over the last axis of x [..., N] (finite values only)."""
     N = x.shape[-1]
     rows = x.numel() // N
-    x = x.contiguous()
+    # rows may sit `ld` apart (a slice of a wider array, e.g. a PeerGather view); anything else is densified
+    ld = x.stride(-2) if x.dim() >= 2 else N
+    uniform = x.stride(-1) == 1 and all(x.stride(d) == x.stride(d + 1) * x.shape[d + 1] for d in range(x.dim() - 2))
+    if not uniform or ld < N:
+        x = x.contiguous()
+        ld = N
     if out is None:
         out = torch.empty((*x.shape[:-1], 3), dtype=torch.float64, device=x.device)
     L = lib()
@@ -275,7 +280,7 @@ def ensemble_stats(x: torch.Tensor, *, out: Optional[torch.Tensor] = None, works
         workspace = Workspace(wsb, x.device)
     ws = workspace.ensure(wsb)
     with torch.cuda.device(x.device):
-        st = L.ens_ensemble_stats(DTYPES[x.dtype], _ptr(x), N, rows, _ptr(out), _ptr(ws), ws.numel(),
+        st = L.ens_ensemble_stats(DTYPES[x.dtype], _ptr(x), N, int(ld), rows, _ptr(out), _ptr(ws), ws.numel(),
                                   _stream_ptr(stream))
     if st:
         raise EnsError(st, "ens_ensemble_stats")

@@ -445,16 +445,16 @@ size_t ens_stats_workspace_bytes(int64_t N, int32_t rows) {
   return align256((size_t)rows * (size_t)cdiv(N, kStatsChunk) * 3 * 8) + 256;
 }
 
-ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int32_t rows, double* stats,
+ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int64_t ld, int32_t rows, double* stats,
                               void* workspace, size_t workspace_bytes, void* stream) {
-  if (!x || !stats || N < 1 || rows < 1 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (!x || !stats || N < 1 || ld < N || rows < 1 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (!workspace || workspace_bytes < ens_stats_workspace_bytes(N, rows)) return ENS_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t nparts = cdiv(N, kStatsChunk);
   const dim3 g((unsigned)nparts, (unsigned)rows);
   double* part = (double*)workspace;
-  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, N, kStatsChunk, part);
-  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, N, kStatsChunk, part);
+  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, ld, kStatsChunk, part);
+  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, ld, kStatsChunk, part);
   stats_merge_kernel<<<rows, 256, 0, s>>>(part, (int)nparts, stats);
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }

@@ -89,3 +89,15 @@ def test_out_ld_slice_equals_contiguous():
     ref = ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, saveat=[0.5, 1.0])
     assert torch.equal(sl, ref.u)
     assert torch.isnan(big[..., :777]).all() and torch.isnan(big[..., 777 + N:]).all()
+
+
+def test_stats_on_row_strided_slice():
+    """ens_ensemble_stats with ld > N (a slice of a wider array) equals the dense computation."""
+    import torch
+
+    import paper_2304_06835_b200 as ens
+    big = torch.randn((2, 3, 10000), dtype=torch.float64, device="cuda")
+    sl = big[..., 1234:1234 + 7000]
+    a = ens.ensemble_stats(sl)
+    b = ens.ensemble_stats(sl.contiguous())
+    assert torch.equal(a, b)
