@@ -15,14 +15,15 @@
 //   std::fma and appears exactly where DESIGN.md §4 (canonical operation order)
 //   puts one; every other operation is a separately rounded IEEE op in T.
 //
-// Pins (tests/test_oracle_*.py, -m "not gpu"): tableau order conditions,
-// stability-polynomial closed forms, convergence orders, Robertson literature
-// values and mass conservation, Philox known-answer vectors, exact discrete
-// EM moments for GBM, LU vs Cramer, model values/Jacobians vs finite
-// differences, stats on exact small cases.
+// Pins (tests/test_oracle_*.py, -m "not gpu"): tableau order conditions
+// (Butcher trees for Tsit5 / Vern7 / Vern9, the Rosenbrock B-series for
+// Rodas4 / Rodas5, dense-output conditions), stability-polynomial closed forms,
+// convergence orders, Robertson and IVP-test-set literature values and
+// invariants, Philox known-answer vectors, the noise-stream structure, exact
+// discrete EM / SIEA moments for GBM, one-step SDE increment moments, LU vs
+// Cramer, model values/Jacobians vs finite differences, stats on exact cases.
 // Parity unpinned (oracle-vs-GPU only): the PI-controller
-// constants (R2) and the stochastic-Lorenz diffusion (R9) — the paper does not
-// print them.
+// constants (R2) — the paper does not print them.
 // =============================================================================
 #include <cmath>
 #include <cstdint>
