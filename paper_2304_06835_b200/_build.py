@@ -63,6 +63,9 @@ def _compile(unit: Path, verbose: bool) -> None:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    # a checkout without the object cache (e.g. the snapshot on a GPU box) keeps an up-to-date library
+    if not force and not OBJ.exists() and LIB.exists() and LIB.stat().st_mtime >= max(p.stat().st_mtime for p in SRCS):
+        return LIB
     OBJ.mkdir(exist_ok=True)
     stamp = OBJ / "flags.txt"
     flags = " ".join([nvcc(), *NVCC_FLAGS])
