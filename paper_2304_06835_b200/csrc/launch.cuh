@@ -62,7 +62,7 @@ inline ens_status launch_status() { return cudaPeekAtLastError() == cudaSuccess 
 template <class Lane, class T, int MINB = 1>
 void launch_adaptive(const Args<T>& a, bool refill, cudaStream_t s) {
   if (refill) {
-    auto kern = adaptive_refill_kernel<Lane, T>;
+    auto kern = adaptive_refill_kernel<Lane, T, MINB>;
     const dim3 b(occupancy_block(kern, a.N));
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)b.x, 0);
