@@ -235,7 +235,7 @@ def main():
         n_l += 1
         if ev_k1 is not None:
             ev_k1.record(stream)
-        ens.ensemble_stats(sol.u.unsqueeze(0), out=st_local, workspace=sws, stream=stream)
+        ens.ensemble_stats(sol.u.unsqueeze(0), out=st_local, workspace=sws, stream=stream, device=dev)
         n_l += 2
         if world > 1:
             g = mg.allgather_stats(st_local)

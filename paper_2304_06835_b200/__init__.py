@@ -262,8 +262,10 @@ def generate_inputs(model: str, recipe: str, N: int, *, dtype=torch.float32, see
 
 
 def ensemble_stats(x: torch.Tensor, *, out: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
-                   stream=None) -> torch.Tensor:
-    """ens_ensemble_stats: (count, mean, M2) over the last axis of x [..., N] (finite values only)."""
+                   stream=None, device=None) -> torch.Tensor:
+    """ens_ensemble_stats: (count, mean, M2) over the last axis of x [..., N] (finite values only).
+    Runs on `device`, else the device of `out`, else x's; x may live on a peer GPU (a PeerGather view),
+    read over NVLink by the executing device."""
     N = x.shape[-1]
     rows = x.numel() // N
     # rows may sit `ld` apart (a slice of a wider array, e.g. a PeerGather view); anything else is densified
@@ -272,14 +274,15 @@ def ensemble_stats(x: torch.Tensor, *, out: Optional[torch.Tensor] = None, works
     if not uniform or ld < N:
         x = x.contiguous()
         ld = N
+    dev = torch.device(device) if device is not None else (out.device if out is not None else x.device)
     if out is None:
-        out = torch.empty((*x.shape[:-1], 3), dtype=torch.float64, device=x.device)
+        out = torch.empty((*x.shape[:-1], 3), dtype=torch.float64, device=dev)
     L = lib()
     wsb = L.ens_stats_workspace_bytes(N, rows)
     if workspace is None:
-        workspace = Workspace(wsb, x.device)
+        workspace = Workspace(wsb, dev)
     ws = workspace.ensure(wsb)
-    with torch.cuda.device(x.device):
+    with torch.cuda.device(dev):
         st = L.ens_ensemble_stats(DTYPES[x.dtype], _ptr(x), N, int(ld), rows, _ptr(out), _ptr(ws), ws.numel(),
                                   _stream_ptr(stream))
     if st:
