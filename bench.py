@@ -212,11 +212,17 @@ def main():
     gather_mode = "none" if (world == 1 or args.no_gather) else args.gather
     peer = None
     if gather_mode == "peer":
+        err = ""
         try:
             peer = mg.PeerGather((3,), N, shard.index_offset, N_total, tdt, dev)
-        except Exception as e:   # IPC mapping unavailable: gather with NCCL after the solve instead
-            print(f"PeerGather unavailable ({e!r}); using the NCCL gather", file=sys.stderr)
-            gather_mode = "nccl"
+        except Exception as e:   # no IPC mapping / peer access: gather with NCCL after the solve instead
+            err = repr(e)
+        # every rank must take the same path
+        flags = [None] * world
+        dist.all_gather_object(flags, err)
+        if any(flags):
+            print(f"PeerGather unavailable ({[f for f in flags if f]}); using the NCCL gather", file=sys.stderr)
+            gather_mode, peer = "nccl", None
     sol = ens.Solution(u=peer.out() if peer is not None else torch.empty((3, N), dtype=tdt, device=dev),
                        retcode=torch.empty(N, dtype=torch.int32, device=dev),
                        n_accept=torch.empty(N, dtype=torch.int32, device=dev),

@@ -112,6 +112,8 @@ class PeerGather:
         else:
             fn, args = payload[0]
             remote = fn(*args)                      # the destination's array, mapped through CUDA IPC
+            if remote.device != self.device and not torch.cuda.can_device_access_peer(self.device, remote.device):
+                raise RuntimeError(f"no peer access {self.device} -> {remote.device}")
         self.view = remote[..., index_offset:index_offset + n_local]
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
 
