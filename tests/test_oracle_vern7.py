@@ -9,7 +9,6 @@ same end time.
 import math
 
 import numpy as np
-import pytest
 
 import oracle
 from tests.order_conditions import rk_max_residual
