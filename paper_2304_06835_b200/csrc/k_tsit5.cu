@@ -37,8 +37,13 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
         const size_t smem = (a.save_grid_only && bulk_saves_ok(a)) ? 2 * M::n * b2.x * 2 * sizeof(float) : 0;
         kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, smem, s>>>(a, cf);
       } else {
-        const dim3 g2((unsigned)cdiv(threads, solver_block(threads))), b2(solver_block(threads));
-        tsit5_fixed_kernel<M, f2, 0><<<g2, b2, 0, s>>>(a, cf);
+        // up to a few waves, the block size with the most resident warps balances the SMs better
+        // (56 registers: 36 warps in 128-thread blocks vs 32 in 256; N = 10^5: 0.45 -> 0.36 ms);
+        // for many waves 256-thread blocks measured 1.4 % faster (profiles/fixed_block_size_r01.jsonl)
+        auto kern = tsit5_fixed_kernel<M, f2, 0>;
+        const bool few_waves = threads < (int64_t)4 * sm_count() * 1024;
+        const dim3 b2(few_waves ? occupancy_block(kern, threads) : solver_block(threads));
+        kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, 0, s>>>(a, cf);
       }
     } else {
       const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
