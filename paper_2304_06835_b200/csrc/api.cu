@@ -226,6 +226,13 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   a.chunk_stride = opt->chunk_stride;
   a.partial = (double*)(ws + L.partial);
   a.counter = (unsigned long long*)(ws + L.counter);
+  std::vector<int64_t> tsit_codes;   // fixed-step Tsit5 save codes (every chunk needs save_grid_only)
+  if (alg == ENS_TSIT5 && !opt->adaptive && a.k > 0) {
+    std::vector<T> tau(a.k);
+    for (int j = 0; j < a.k; ++j) tau[j] = (T)opt->saveat[j];
+    fixed_save_codes<T>(t0, tf, dt, nsteps, tau, tsit_codes);
+    a.save_grid_only = std::all_of(tsit_codes.begin(), tsit_codes.end(), [](int64_t c) { return (c & 1) == 0; });
+  }
   if (stage_ws) {
     if (a.k > 0) {
       std::vector<T> tau(a.k);
@@ -238,10 +245,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
         if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return ENS_E_CUDA;
       } else if (alg == ENS_TSIT5 && !opt->adaptive) {
-        std::vector<int64_t> st;
-        fixed_save_codes<T>(t0, tf, dt, nsteps, tau, st);
-        a.save_grid_only = std::all_of(st.begin(), st.end(), [](int64_t c) { return (c & 1) == 0; });
-        if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        if (cudaMemcpyAsync(ws + L.save_step, tsit_codes.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return ENS_E_CUDA;
       }
     }
