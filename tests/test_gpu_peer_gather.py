@@ -100,3 +100,29 @@ def test_stats_on_row_strided_slice():
     a = ens.ensemble_stats(sl)
     b = ens.ensemble_stats(sl.contiguous())
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("model,alg,kw", [("gbm", "em", dict(seed=3)), ("robertson", "rodas5", dict(adaptive=True)),
+                                          ("lorenz", "vern9", dict(adaptive=True))])
+def test_out_ld_all_kernel_families(model, alg, kw):
+    """out_ld on the SDE, Rosenbrock and Verner kernels (stats on for EM: the fused partials
+    read the states in registers, the slice only receives them)."""
+    import torch
+
+    import paper_2304_06835_b200 as ens
+    N = 1000
+    u0, p = ens.generate_inputs(model, "random10", N, dtype=torch.float64, seed=8)
+    n = u0.shape[0]
+    big = torch.full((2, n, 2500), float("nan"), dtype=torch.float64, device="cuda")
+    sl = big[..., 300:300 + N]
+    sa = [0.0, 0.5] if alg == "em" else [0.5, 1.0]
+    out = ens.Solution(u=sl, retcode=torch.empty(N, dtype=torch.int32, device="cuda"),
+                       n_accept=torch.empty(N, dtype=torch.int32, device="cuda"),
+                       n_reject=torch.empty(N, dtype=torch.int32, device="cuda"),
+                       stats=torch.empty((2, n, 3), dtype=torch.float64, device="cuda") if alg == "em" else None)
+    ens.solve(model, alg, u0, p, (0.0, 1.0), 0.01, saveat=sa, out=out, stats=(alg == "em"), **kw)
+    ref = ens.solve(model, alg, u0, p, (0.0, 1.0), 0.01, saveat=sa, stats=(alg == "em"), **kw)
+    assert torch.equal(sl, ref.u)
+    if alg == "em":
+        assert torch.equal(out.stats, ref.stats)
+    assert torch.isnan(big[..., :300]).all() and torch.isnan(big[..., 300 + N:]).all()
