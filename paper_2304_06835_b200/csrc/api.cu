@@ -217,7 +217,8 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   a.nsteps = nsteps; a.h_last = (T)hl;
   a.dt0 = opt->adaptive ? (T)std::min(dt, tf - t0) : (T)dt;
   a.abstol = (T)opt->abstol; a.reltol = (T)opt->reltol;
-  a.max_steps = opt->max_steps > 0 ? opt->max_steps : 1000000;
+  // attempts = n_accept + n_reject (int32 counters), so a cap above INT32_MAX is unreachable
+  a.max_steps = (int32_t)std::min<int64_t>(opt->max_steps > 0 ? opt->max_steps : 1000000, INT32_MAX);
   a.k = opt->n_saveat;
   a.tau = (const T*)(ws + L.tau);
   a.save_step = (const int64_t*)(ws + L.save_step);

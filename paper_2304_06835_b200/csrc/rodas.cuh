@@ -173,13 +173,12 @@ template <class M, class T, bool SAVE> struct Rodas4Lane {
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret, js;
-  int64_t attempts;
   bool done;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
     t = a.t0; h = a.dt0; lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
     M::f(u, par, t, F0);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -189,10 +188,9 @@ template <class M, class T, bool SAVE> struct Rodas4Lane {
   }
 
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (attempts >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
     const bool last = (t + h >= a.tf);
     if (last) h = a.tf - t;
-    ++attempts;
     T un[n], K[6][n];
     if (!rodas_step<Rodas4Tab, M, T>(par, t, h, u, F0, un, K)) {
       h = h * T(0.5);                       // singular W: reject and halve (DESIGN R10)
@@ -285,13 +283,12 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;
   int32_t nacc, nrej, ret, js;
-  int64_t attempts;
   bool done;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
     t = a.t0; h = a.dt0; lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
     M::f(u, par, t, F0);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -301,11 +298,10 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
   }
 
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (attempts >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
     const T target = (SAVE && js < a.k) ? __ldg(a.tau + js) : a.tf;
     const bool clip = (t + h >= target);
     if (clip) h = target - t;
-    ++attempts;
     T un[n], K[Tab::S][n];
     if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) {
       h = h * T(0.5);                       // singular W: reject and halve (DESIGN R10)

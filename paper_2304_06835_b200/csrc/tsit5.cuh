@@ -386,7 +386,6 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
   T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret;
   int32_t js;
-  int64_t attempts;
   bool done;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
@@ -394,7 +393,7 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     t = a.t0;
     h = a.dt0;                 // (T)min(dt, tf − t0), computed on the host in fp64
     lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
     M::f(u, par, t, K[0]);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -405,7 +404,7 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
 
   // One attempted step: stages, error, q, accept/reject, PI.
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (attempts >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
     const bool last = (t + h >= a.tf);
     if (last) h = a.tf - t;
     T y[n], E[n];
@@ -413,7 +412,6 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
     tsit5_stages<M, T>(par, t, h, ha, u, K, y);
     tsit5_error<n, T>(h, K, E);
     const T q2 = error_q2<n, T>(E, u, y, a.abstol, a.reltol);
-    ++attempts;
     if (q2 < T(1)) {
       T tn = last ? a.tf : t + h;
       bool event = false;

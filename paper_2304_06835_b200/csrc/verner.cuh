@@ -141,13 +141,12 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret, js;
-  int64_t attempts;
   bool done;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
     t = a.t0; h = a.dt0; lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; attempts = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
     M::f(u, par, t, F0);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -157,7 +156,7 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   }
 
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (attempts >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
     const T target = (SAVE && js < a.k) ? __ldg(a.tau + js) : a.tf;   // next save point or tf (R21)
     const bool clip = (t + h >= target);
     if (clip) h = target - t;
@@ -166,7 +165,6 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
     for (int c = 0; c < n; ++c) K[0][c] = F0[c];
     verner_step<Tab, M, T, true>(par, t, h, u, K, un, E);
     const T q2 = error_q2<n, T>(E, u, un, a.abstol, a.reltol);
-    ++attempts;
     if (q2 < T(1)) {
       t = clip ? target : t + h;
 #pragma unroll
