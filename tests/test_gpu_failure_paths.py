@@ -43,3 +43,18 @@ def test_max_steps(alg):
     assert (rc == 1).all() and ((na + nr) == 7).all()
     np.testing.assert_array_equal(na, ona)
     assert traj_relerr(g, o).max() <= 1e-12
+
+
+@pytest.mark.parametrize("alg", ["tsit5", "rosenbrock23"])
+def test_max_steps_above_int32(alg):
+    """Attempts are counted as n_accept + n_reject (int32); a cap above INT32_MAX is
+    clamped on the host and behaves as "no cap reached" — same results as the oracle
+    with the 64-bit cap (step counters)."""
+    u0, p = make_inputs("lorenz", "random10", 64, seed=3, dtype="f64")
+    kw = dict(adaptive=True, abstol=1e-8, reltol=1e-8, max_steps=1 << 40)
+    g, rc, na, nr, _ = gpu("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, **kw)
+    o, orc, ona, onr = oracle.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, dtype="f64", **kw)
+    assert (rc == 0).all() and (orc == 0).all()
+    np.testing.assert_array_equal(na, ona)
+    np.testing.assert_array_equal(nr, onr)
+    assert traj_relerr(g, o).max() <= 1e-8
