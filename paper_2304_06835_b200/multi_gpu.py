@@ -144,3 +144,79 @@ def gather_states(local: torch.Tensor, dst: int = 0, group=None) -> Optional[tor
         return torch.stack(bufs).to(local.device)
     dist.gather(src, dst=dst, group=group)
     return None
+
+
+@dataclass
+class MultiSolution:
+    """Result of `solve` on one rank."""
+    shard: Shard
+    local: "object"                      # this rank's ens.Solution (u may be a view into dst's gather array)
+    stats: Optional[torch.Tensor]        # merged [max(k,1), n, 3] (count, mean, M2) on every rank, or None
+    gathered: Optional[torch.Tensor]     # on dst: [*lead, N_total] in global order (gather="peer"), or
+    #                                      [R, *lead, N_r] rank blocks (gather="nccl"); None elsewhere / no gather
+
+
+def solve(model: str, alg: str, recipe: str, N_total: int, tspan, dt, *, dtype=torch.float32, input_seed: int = 0,
+          shard: str = "auto", chunk: int = 1 << 16, gather: Optional[str] = None, dst: int = 0, stats: bool = False,
+          saveat=None, group=None, device=None, **solve_kw) -> MultiSolution:
+    """The multi-rank driver (SURVEY §8b `ens.multi_gpu.solve`, §8e): call on every rank of an
+    initialised process group, one rank per GPU.
+
+    1. shard the N_total trajectories: "contiguous", "block_cyclic" (chunks of `chunk` dealt round-robin,
+       one launch per rank through ens_options.chunk_len / chunk_stride), or "auto" (block-cyclic for
+       adaptive runs when N_total divides evenly, contiguous otherwise);
+    2. generate this shard's inputs on the rank's GPU from (input_seed, global index) — no scatter;
+    3. solve the shard (global indices key the Philox noise, so every trajectory is bit-identical for
+       any world size);
+    4. stats=True: per-rank (count, mean, M2) — fused in the EM kernels, a reduction pass over the
+       stored states otherwise — all-gathered and merged in fixed rank order on every rank;
+    5. gather="peer": the solver stores straight into dst's [*lead, N_total] array (PeerGather; contiguous
+       shards only); gather="nccl": NCCL gather of the rank blocks after the solve (equal N_r).
+    `solve_kw` goes to ens.solve (adaptive, abstol, reltol, seed, refill, max_steps, ...)."""
+    import paper_2304_06835_b200 as ens
+    R, me = dist.get_world_size(group), dist.get_rank(group)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    adaptive = bool(solve_kw.get("adaptive", False))
+    if shard == "auto":
+        shard = "block_cyclic" if adaptive and N_total % (chunk * R) == 0 else "contiguous"
+    if shard == "block_cyclic":
+        if gather == "peer":
+            raise ValueError("gather='peer' needs contiguous shards")
+        sh = shard_block_cyclic(N_total, me, R, chunk)
+    elif shard == "contiguous":
+        sh = shard_contiguous(N_total, me, R)
+    else:
+        raise ValueError(f"unknown shard layout {shard!r}")
+    if gather == "nccl" and N_total % R != 0:
+        raise ValueError("gather='nccl' needs equal shards (N_total divisible by the world size)")
+    if gather not in (None, "peer", "nccl"):
+        raise ValueError(f"unknown gather {gather!r}")
+
+    u0, p = ens.generate_inputs(model, recipe, sh.n_local, dtype=dtype, seed=input_seed, index_offset=sh.index_offset,
+                                N_total=N_total, chunk_len=sh.chunk_len, chunk_stride=sh.chunk_stride, device=dev)
+    n, _, _ = ens.model_dims(model)
+    k = 0 if saveat is None else len(saveat)
+    lead = (k, n) if k else (n,)
+    sde = alg in ("em", "siea")
+    pg = PeerGather(lead, sh.n_local, sh.index_offset, N_total, dtype, dev, dst=dst, group=group) \
+        if gather == "peer" else None
+    out = None
+    if pg is not None:
+        out = ens.Solution(u=pg.out(), retcode=torch.empty(sh.n_local, dtype=torch.int32, device=dev),
+                           n_accept=torch.empty(sh.n_local, dtype=torch.int32, device=dev),
+                           n_reject=torch.empty(sh.n_local, dtype=torch.int32, device=dev),
+                           stats=torch.empty((max(k, 1), n, 3), dtype=torch.float64, device=dev)
+                           if (stats and sde) else None)
+    sol = ens.solve(model, alg, u0, p, tspan, dt, saveat=saveat, stats=stats and sde, out=out,
+                    store_states=(gather is not None) or not (stats and sde),
+                    index_offset=sh.index_offset, chunk_len=sh.chunk_len, chunk_stride=sh.chunk_stride, **solve_kw)
+    merged = None
+    if stats:
+        st = sol.stats if sde else ens.ensemble_stats(sol.u if k else sol.u.unsqueeze(0), device=dev)
+        merged = merge_stats(allgather_stats(st, group))
+    gathered = None
+    if pg is not None:
+        gathered = pg.complete()
+    elif gather == "nccl":
+        gathered = gather_states(sol.u, dst=dst, group=group)
+    return MultiSolution(sh, sol, merged, gathered)

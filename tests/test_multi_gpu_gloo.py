@@ -53,6 +53,14 @@ def _worker(rank, world, port, q):
             ug, pg = make_inputs("lorenz", "random10", N_total, seed=0xC5)
             gi = sh.global_indices().numpy()
             assert np.array_equal(p, pg[:, gi]) and np.array_equal(u0, ug[:, gi])
+        # multi_gpu.solve rejects inconsistent layouts before any device work
+        for kw, msg in [(dict(shard="block_cyclic", gather="peer"), "contiguous"),
+                        (dict(shard="diagonal"), "unknown shard"),
+                        (dict(gather="allgather"), "unknown gather")]:
+            with pytest.raises(ValueError, match=msg):
+                mg.solve("lorenz", "tsit5", "random10", world * 4096, (0.0, 1.0), 1e-3, device="cpu", **kw)
+        with pytest.raises(ValueError, match="equal shards"):
+            mg.solve("lorenz", "tsit5", "random10", world * 4096 + 1, (0.0, 1.0), 1e-3, gather="nccl", device="cpu")
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
