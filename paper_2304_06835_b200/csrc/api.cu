@@ -329,9 +329,22 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   const size_t ts = dtype == ENS_F32 ? 4 : 8;
   const int kk = std::max(1, opt->n_saveat);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaStream_t sh = nullptr, sd = nullptr;
+  cudaStream_t sh = nullptr, sd = nullptr, s2 = nullptr;
   if (cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking) != cudaSuccess) return ENS_E_CUDA;
   if (cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) != cudaSuccess) { cudaStreamDestroy(sh); return ENS_E_CUDA; }
+  // Odd chunks solve on a second compute stream, so a chunk's kernel fills the
+  // SMs its predecessor's last partial wave leaves idle (one stream would
+  // serialise the launches and expose every chunk's tail). Not with refill: its
+  // per-launch queue counter lives in the shared workspace.
+  const bool dual = C > 1 && !(opt->adaptive && opt->refill);
+  if (dual && cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaStreamDestroy(sh); cudaStreamDestroy(sd); return ENS_E_CUDA;
+  }
+  cudaEvent_t staged = nullptr, s2_done = nullptr;
+  if (dual) {
+    cudaEventCreateWithFlags(&staged, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&s2_done, cudaEventDisableTiming);
+  }
   std::vector<cudaEvent_t> ev_in(C), ev_out(C);
   for (int64_t c = 0; c < C; ++c) {
     cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming);
@@ -359,18 +372,21 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
                               cudaMemcpyHostToDevice, sh) == cudaSuccess;
     }
     cudaEventRecord(ev_in[c], sh);
-    cudaStreamWaitEvent(s, ev_in[c], 0);
+    cudaStream_t cs = (dual && (c & 1)) ? s2 : s;
+    if (dual && c == 1) cudaStreamWaitEvent(s2, staged, 0);   // after chunk 0 staged saveat into the workspace
+    cudaStreamWaitEvent(cs, ev_in[c], 0);
     out.u_out = (char*)d_u_out + lo * ts;
     out.retcode = d_retcode ? d_retcode + lo : nullptr;
     ens_options o = *opt;
     if (o.chunk_len == 0) o.index_offset = opt->index_offset + lo;
     const void* pp = opt->p_broadcast ? d_p : (const void*)((const char*)d_p + lo * ts);
     if (dtype == ENS_F32)
-      st = solve_impl<float>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, s, c == 0);
+      st = solve_impl<float>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, cs, c == 0);
     else
-      st = solve_impl<double>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, s, c == 0);
+      st = solve_impl<double>(model, alg, len, N, (const char*)d_u0 + lo * ts, pp, t0, tf, dt, &o, &out, n, cs, c == 0);
     if (st != ENS_OK) { ok = false; break; }
-    cudaEventRecord(ev_out[c], s);
+    if (dual && c == 0) cudaEventRecord(staged, s);
+    cudaEventRecord(ev_out[c], cs);
     cudaStreamWaitEvent(sd, ev_out[c], 0);
     ok &= cudaMemcpy2DAsync((char*)u_out_host + lo * ts, N * ts, (const char*)d_u_out + lo * ts, N * ts, len * ts,
                             (size_t)kk * n, cudaMemcpyDeviceToHost, sd) == cudaSuccess;
@@ -378,9 +394,18 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
       ok &= cudaMemcpyAsync(retcode_host + lo, d_retcode + lo, len * 4, cudaMemcpyDeviceToHost, sd) == cudaSuccess;
     lo += len;
   }
+  if (dual) {                                // the caller's stream orders after every chunk
+    cudaEventRecord(s2_done, s2);
+    cudaStreamWaitEvent(s, s2_done, 0);
+  }
   ok &= cudaStreamSynchronize(sd) == cudaSuccess;
   ok &= cudaStreamSynchronize(s) == cudaSuccess;
   cudaStreamSynchronize(sh);
+  if (dual) {
+    cudaEventDestroy(staged);
+    cudaEventDestroy(s2_done);
+    cudaStreamDestroy(s2);
+  }
   for (int64_t c = 0; c < C; ++c) { cudaEventDestroy(ev_in[c]); cudaEventDestroy(ev_out[c]); }
   cudaEventDestroy(start);
   cudaStreamDestroy(sh);
