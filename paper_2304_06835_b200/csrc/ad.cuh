@@ -71,22 +71,33 @@ template <class T, int N> __device__ __forceinline__ Dual<T, N> operator-(T s, c
   return r;
 }
 
-// J[i][k] = ∂f_i/∂y_k by one dual evaluation with seeds y_i.d[k] = δ_ik.
+// J[i][k] = ∂f_i/∂y_k. Every partial is computed by its own chain of the rules
+// above, independent of the other partials, so the columns may be produced in
+// passes of W seeds each (W = n: one evaluation with unit seeds) with identical
+// results. Small systems take one pass; for n > 4 the n-wide duals of every
+// intermediate overflow the register file (POLLU: 17.7 KB of local memory per
+// thread), so the columns are formed in passes of kAdPass<n> seeds.
+template <int n> constexpr int kAdPass = (n <= 4) ? n : 1;
+
 template <class M, class T>
 __device__ __forceinline__ void ad_jacobian(const T (&u)[M::n], const T (&p)[M::m], T t, T (&J)[M::n][M::n]) {
-  constexpr int n = M::n;
-  Dual<T, n> y[n], o[n];
+  constexpr int n = M::n, W = kAdPass<n>;
+  static_assert(n % W == 0, "AD pass width must divide n");
+#pragma unroll (n <= 8 ? n / W : 1)
+  for (int k0 = 0; k0 < n; k0 += W) {
+    Dual<T, W> y[n], o[n];
 #pragma unroll (n <= 8 ? n : 1)
-  for (int i = 0; i < n; ++i) {
-    y[i].v = u[i];
+    for (int i = 0; i < n; ++i) {
+      y[i].v = u[i];
+#pragma unroll
+      for (int c = 0; c < W; ++c) y[i].d[c] = (i == k0 + c) ? T(1) : T(0);
+    }
+    M::f(y, p, t, o);
 #pragma unroll (n <= 8 ? n : 1)
-    for (int k = 0; k < n; ++k) y[i].d[k] = (i == k) ? T(1) : T(0);
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int c = 0; c < W; ++c) J[i][k0 + c] = o[i].d[c];
   }
-  M::f(y, p, t, o);
-#pragma unroll (n <= 8 ? n : 1)
-  for (int i = 0; i < n; ++i)
-#pragma unroll (n <= 8 ? n : 1)
-    for (int k = 0; k < n; ++k) J[i][k] = o[i].d[k];
 }
 
 }  // namespace ens
