@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
         L.ens_sde_noise.restype = i32
         L.ens_philox4x32_10.argtypes = [vp, vp, vp, i64, vp]
         L.ens_philox4x32_10.restype = i32
+        L.ens_check_log2_quotient.argtypes = [vp, vp]
+        L.ens_check_log2_quotient.restype = i32
         L.ens_status_string.argtypes = [i32]
         L.ens_status_string.restype = ctypes.c_char_p
         L.ens_version.restype = ctypes.c_char_p
@@ -93,8 +95,8 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTS = ["ens_model_dims", "ens_workspace_bytes", "ensemble_solve", "ensemble_solve_host", "ens_generate_inputs",
-           "ens_ensemble_stats", "ens_stats_workspace_bytes", "ens_stats_finalize", "ens_stats_merge", "ens_sde_noise", "ens_philox4x32_10", "ens_status_string",
-           "ens_version"]
+           "ens_ensemble_stats", "ens_stats_workspace_bytes", "ens_stats_finalize", "ens_stats_merge", "ens_sde_noise", "ens_philox4x32_10", "ens_check_log2_quotient",
+           "ens_status_string", "ens_version"]
 
 
 def status_string(status: int) -> str:
@@ -329,6 +331,18 @@ def sde_noise(N: int, nsteps: int, *, seed: int, dtype=torch.float32, step0: int
     if st:
         raise EnsError(st, "ens_sde_noise")
     return words, z
+
+
+def check_log2_quotient(device=None) -> int:
+    """ens_check_log2_quotient: number of fp32 m in [√½, √2) where the log2 polynomial's quotient
+    (reciprocal + refinement) differs from IEEE division (0 = identical everywhere)."""
+    dev = torch.device(device or "cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        st = lib().ens_check_log2_quotient(_ptr(cnt), None)
+    if st:
+        raise EnsError(st, "ens_check_log2_quotient")
+    return int(cnt.item())
 
 
 def philox4x32_10(ctr: torch.Tensor, key: torch.Tensor, stream=None) -> torch.Tensor:
