@@ -214,14 +214,16 @@ ens_status ens_sde_noise(ens_dtype dtype, uint64_t seed, int64_t N, int64_t step
  * i < N; ctr/out device uint32 [N][4], key device uint32 [N][2]. */
 ens_status ens_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int64_t N, void* stream);
 
-/* Self-check of an implementation shortcut: the fp32 quotient
- * s = (m − 1)/(m + 1) of the log2 polynomial (controller R2, Box–Muller R8) is
- * computed as reciprocal + refinement without IEEE division's range check.
- * Compares it, on the device, with IEEE division for every fp32 m in
- * [√½, √2) (8,388,608 values, scalar and packed forms); *mismatches (device
- * uint64, caller-owned) receives the number of differing results — 0 means
- * bit-identical on the whole range. Asynchronous on `stream`. */
-ens_status ens_check_log2_quotient(unsigned long long* mismatches, void* stream);
+/* Self-check of two implementation shortcuts of the packed fp32 Box–Muller
+ * (DESIGN §5): the log2 polynomial's quotient s = (m − 1)/(m + 1) (R2, R8) as
+ * reciprocal + refinement, and the radius √x as reciprocal square root +
+ * refinement, both without the IEEE operations' range checks. Compares them on
+ * the device with IEEE division / sqrt for every fp32 m in [√½, √2)
+ * (8,388,608 values) and every fp32 x in [1e-7, 64) (about 2.6e8 values).
+ * mismatches: device uint64[2], caller-owned; receives the number of differing
+ * results of each check — 0 means bit-identical on the whole range.
+ * Asynchronous on `stream`. */
+ens_status ens_check_fast_paths(unsigned long long* mismatches, void* stream);
 
 /* Human-readable status. */
 const char* ens_status_string(ens_status s);

@@ -85,8 +85,8 @@ def lib() -> ctypes.CDLL:
         L.ens_sde_noise.restype = i32
         L.ens_philox4x32_10.argtypes = [vp, vp, vp, i64, vp]
         L.ens_philox4x32_10.restype = i32
-        L.ens_check_log2_quotient.argtypes = [vp, vp]
-        L.ens_check_log2_quotient.restype = i32
+        L.ens_check_fast_paths.argtypes = [vp, vp]
+        L.ens_check_fast_paths.restype = i32
         L.ens_status_string.argtypes = [i32]
         L.ens_status_string.restype = ctypes.c_char_p
         L.ens_version.restype = ctypes.c_char_p
@@ -95,7 +95,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTS = ["ens_model_dims", "ens_workspace_bytes", "ensemble_solve", "ensemble_solve_host", "ens_generate_inputs",
-           "ens_ensemble_stats", "ens_stats_workspace_bytes", "ens_stats_finalize", "ens_stats_merge", "ens_sde_noise", "ens_philox4x32_10", "ens_check_log2_quotient",
+           "ens_ensemble_stats", "ens_stats_workspace_bytes", "ens_stats_finalize", "ens_stats_merge", "ens_sde_noise", "ens_philox4x32_10", "ens_check_fast_paths",
            "ens_status_string", "ens_version"]
 
 
@@ -333,16 +333,16 @@ def sde_noise(N: int, nsteps: int, *, seed: int, dtype=torch.float32, step0: int
     return words, z
 
 
-def check_log2_quotient(device=None) -> int:
-    """ens_check_log2_quotient: number of fp32 m in [√½, √2) where the log2 polynomial's quotient
-    (reciprocal + refinement) differs from IEEE division (0 = identical everywhere)."""
+def check_fast_paths(device=None):
+    """ens_check_fast_paths: (mismatches of the log2 quotient over fp32 m in [√½, √2),
+    mismatches of the Box–Muller sqrt over fp32 x in [1e-7, 64)) against IEEE division / sqrt."""
     dev = torch.device(device or "cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     with torch.cuda.device(dev):
-        st = lib().ens_check_log2_quotient(_ptr(cnt), None)
+        st = lib().ens_check_fast_paths(_ptr(cnt), None)
     if st:
-        raise EnsError(st, "ens_check_log2_quotient")
-    return int(cnt.item())
+        raise EnsError(st, "ens_check_fast_paths")
+    return tuple(int(v) for v in cnt.tolist())
 
 
 def philox4x32_10(ctr: torch.Tensor, key: torch.Tensor, stream=None) -> torch.Tensor:

@@ -526,12 +526,14 @@ ens_status ens_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t*
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 
-ens_status ens_check_log2_quotient(unsigned long long* mismatches, void* stream) {
+ens_status ens_check_fast_paths(unsigned long long* mismatches, void* stream) {
   if (!mismatches) return ENS_E_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(mismatches, 0, sizeof(unsigned long long), s) != cudaSuccess) return ENS_E_CUDA;
+  if (cudaMemsetAsync(mismatches, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) return ENS_E_CUDA;
   // m ∈ [(float)√½, 2·(float)√½): every m that L(x) forms (frexp mantissa, doubled below √½)
   log2_quot_check_kernel<<<4 * sm_count(), kBlock, 0, s>>>(0x3F3504F3u, 0x3FB504F3u, mismatches);
+  // x ∈ [1e-7, 64): every Box–Muller radicand −2 ln U of the fp32 uniforms
+  bm_sqrt_check_kernel<<<8 * sm_count(), kBlock, 0, s>>>(0x33D6BF95u, 0x42800000u, mismatches + 1);
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }
 
