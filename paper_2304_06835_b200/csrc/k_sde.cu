@@ -15,8 +15,13 @@ ens_status run_sde(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       return ENS_E_UNSUPPORTED;
     }
   } else {
-    if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
-    else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    if constexpr (sizeof(T) == 8 && M::nw > 3) {   // fp64 CRN: three blocks per SM (em_kernel_b3)
+      if (opt->want_stats) em_kernel_b3<M, T, true><<<g, b, 0, s>>>(a);
+      else em_kernel_b3<M, T, false><<<g, b, 0, s>>>(a);
+    } else {
+      if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
+      else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    }
   }
   return launch_status();
 }
