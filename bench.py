@@ -226,10 +226,12 @@ def main():
     sol = ens.Solution(u=peer.out() if peer is not None else torch.empty((3, N), dtype=tdt, device=dev),
                        retcode=torch.empty(N, dtype=torch.int32, device=dev),
                        n_accept=torch.empty(N, dtype=torch.int32, device=dev),
-                       n_reject=torch.empty(N, dtype=torch.int32, device=dev), stats=None)
-    ws = ens.Workspace(ens.workspace_bytes("lorenz", "tsit5", tdt, N), dev)
-    sws = ens.Workspace(ens.lib().ens_stats_workspace_bytes(N, 3), dev)
-    st_local = torch.empty((1, 3, 3), dtype=torch.float64, device=dev)
+                       n_reject=torch.empty(N, dtype=torch.int32, device=dev),
+                       stats=torch.empty((1, 3, 3), dtype=torch.float64, device=dev))
+    st_local = sol.stats
+    # a12 fused into the solve: each warp's final states reduced to (count, mean, M2) in the kernel
+    # epilogue, one merge kernel after (no pass over the stored states, which on N>1 live on rank 0)
+    ws = ens.Workspace(ens.workspace_bytes("lorenz", "tsit5", tdt, N, stats=True), dev)
     stream = torch.cuda.current_stream(dev)
     launches_per_step = [0]
 
@@ -237,12 +239,10 @@ def main():
         n_l = 0
         if ev_k0 is not None:
             ev_k0.record(stream)
-        ens.solve("lorenz", "tsit5", u0, p, tspan, dt, workspace=ws, out=sol, stream=stream)
-        n_l += 1
+        ens.solve("lorenz", "tsit5", u0, p, tspan, dt, stats=True, workspace=ws, out=sol, stream=stream)
+        n_l += 2        # solve kernel (with the fused statistics partials) + stats merge kernel
         if ev_k1 is not None:
             ev_k1.record(stream)
-        ens.ensemble_stats(sol.u.unsqueeze(0), out=st_local, workspace=sws, stream=stream, device=dev)
-        n_l += 2
         if world > 1:
             g = mg.allgather_stats(st_local)
             mg.merge_stats(g)
@@ -390,7 +390,7 @@ def main():
                                    f"point, N=10^7 per GPU)",
                        "N_per_gpu": N, "N_total": N_total, "tspan": [0.0, 1.0], "dt": dt, "nsteps": nsteps,
                        "parallelism": f"dp{world} (trajectory shards)", "l2": "inputs+outputs (360 MB) > L2 (126 MB)",
-                       "step": "ensemble_solve + ensemble_stats" + (" + NCCL allgather(stats)+merge" +
+                       "step": "ensemble_solve with fused ensemble statistics" + (" + NCCL allgather(stats)+merge" +
                                                                     {"none": "", "nccl": " + NCCL gather(states)", "peer": " (states stored into rank 0's array by the solve: fused peer gather)"}[gather_mode]
                                                                     if world > 1 else "")},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -84,10 +84,15 @@ void fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last
 }
 
 struct Layout {
-  size_t counter, tau, save_step, partial, total;
+  size_t counter, tau, save_step, partial, partial2, total;
   int64_t nparts;
   int rows;
 };
+
+// Statistics computed inside the solve kernel from registers (no pass over the stored states).
+bool fused_stats(int alg, const ens_options* opt) {
+  return opt && opt->want_stats && alg == ENS_TSIT5 && !opt->adaptive && opt->n_saveat == 0;
+}
 
 Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
   Layout L{};
@@ -101,8 +106,11 @@ Layout layout(int n, int alg, int dtype, int64_t N, const ens_options* opt) {
   const bool stats = opt && opt->want_stats;
   L.nparts = 0;
   // EM: one partial per solver block; sized for the smallest block (32) so the layout is device independent
-  if (stats) L.nparts = is_sde_alg(alg) ? cdiv(N, 32) : cdiv(N, kStatsChunk);
-  L.total = L.partial + align256((size_t)L.rows * (size_t)L.nparts * 3 * 8) + 256;
+  // fixed-step Tsit5 without saves: one partial per warp, fused into the solve (tsit5_fixed_kernel STATS)
+  if (stats) L.nparts = (is_sde_alg(alg) || fused_stats(alg, opt)) ? cdiv(N, 32) : cdiv(N, kStatsChunk);
+  L.partial2 = L.partial + align256((size_t)L.rows * (size_t)L.nparts * 3 * 8);
+  // first-stage merge outputs (stats_fold_kernel) when there are many partials
+  L.total = L.partial2 + align256((size_t)L.rows * (size_t)cdiv(L.nparts, 256 * kFold) * 3 * 8) + 256;
   return L;
 }
 
@@ -257,12 +265,22 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   ens_status st = dispatch<T>(model, alg, a, opt, s);
   if (st != ENS_OK) return st;
   if (opt->want_stats) {
-    if (!is_sde_alg(alg)) {
+    const bool fused = fused_stats(alg, opt);
+    if (!is_sde_alg(alg) && !fused) {
       const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
       stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, a.ldo, kStatsChunk, a.partial);
     }
-    const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for(N).x : L.nparts;
-    stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
+    // EM: one partial per block; fused Tsit5: one per warp (two trajectories per lane in fp32)
+    const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for(N).x
+                           : fused ? cdiv(N, 32 * (sizeof(T) == 4 ? 2 : 1)) : L.nparts;
+    if (nparts > 4 * 256 * kFold) {   // many partials (fused per-warp stats): fold in parallel first
+      double* p2 = (double*)(ws + L.partial2);
+      const int64_t nblk = cdiv(nparts, 256 * kFold);
+      stats_fold_kernel<<<dim3((unsigned)nblk, (unsigned)L.rows), 256, 0, s>>>(a.partial, nparts, p2);
+      stats_merge_kernel<<<L.rows, 256, 0, s>>>(p2, (int)nblk, out->stats);
+    } else {
+      stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
+    }
     if (cudaPeekAtLastError() != cudaSuccess) return ENS_E_CUDA;
   }
   return ENS_OK;

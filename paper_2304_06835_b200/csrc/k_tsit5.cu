@@ -40,7 +40,7 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
         // up to a few waves, the block size with the most resident warps balances the SMs better
         // (56 registers: 36 warps in 128-thread blocks vs 32 in 256; N = 10^5: 0.45 -> 0.36 ms);
         // for many waves 256-thread blocks measured 1.4 % faster (profiles/fixed_block_size_r01.jsonl)
-        auto kern = tsit5_fixed_kernel<M, f2, 0>;
+        auto kern = opt->want_stats ? tsit5_fixed_kernel<M, f2, 0, true> : tsit5_fixed_kernel<M, f2, 0>;
         const bool few_waves = threads < (int64_t)4 * sm_count() * 1024;
         const dim3 b2(few_waves ? occupancy_block(kern, threads) : solver_block(threads));
         kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, 0, s>>>(a, cf);
@@ -55,7 +55,8 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
         kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, smem, s>>>(a, cf);
       } else {
         const dim3 g = grid_for(a.N), b(solver_block(a.N));
-        tsit5_fixed_kernel<M, double, 0><<<g, b, 0, s>>>(a, cf);
+        if (opt->want_stats) tsit5_fixed_kernel<M, double, 0, true><<<g, b, 0, s>>>(a, cf);
+        else tsit5_fixed_kernel<M, double, 0><<<g, b, 0, s>>>(a, cf);
       }
     }
   } else {

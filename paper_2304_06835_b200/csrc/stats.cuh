@@ -43,6 +43,26 @@ __device__ __forceinline__ void block_stats_partial(double* red, bool valid, dou
   if (threadIdx.x == 0) { out3[0] = c; out3[1] = mean; out3[2] = m2; }
 }
 
+// Two-pass (count, mean, M2) of a warp's finite values, W per lane (fixed-step
+// Tsit5 epilogue: fused statistics of the final states, one partial per warp);
+// lane 0 writes out3. Every lane of the warp must call it.
+template <int W>
+__device__ __forceinline__ void warp_stats_partial(const bool (&use)[W], const double (&x)[W], double* out3) {
+  double c = 0.0, s = 0.0;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (use[w]) { c += 1.0; s += x[w]; }
+  c = warp_sum(c);
+  s = warp_sum(s);
+  const double mean = c > 0.0 ? s / c : 0.0;
+  double m2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (use[w]) { const double d = x[w] - mean; m2 = fma(d, d, m2); }
+  m2 = warp_sum(m2);
+  if ((threadIdx.x & 31) == 0) { out3[0] = c; out3[1] = mean; out3[2] = m2; }
+}
+
 struct Moments { double c, mean, m2; };
 
 // Chan et al. pairwise combination of (count, mean, M2).
@@ -107,6 +127,39 @@ static __global__ void __launch_bounds__(256) stats_merge_kernel(const double* _
     __syncthreads();
   }
   if (threadIdx.x == 0) { out[row * 3] = sc[0]; out[row * 3 + 1] = sm[0]; out[row * 3 + 2] = s2[0]; }
+}
+
+// First stage of a two-stage merge for many partials (fused per-warp
+// statistics: N/64 partials per row): grid (nblk, rows); block b folds partials
+// [b·256·kFold, (b+1)·256·kFold) of its row — thread t folds kFold consecutive
+// partials in order, then the block's fixed binary tree — into out
+// [rows][nblk][3], which stats_merge_kernel then merges. Fixed order throughout.
+constexpr int kFold = 8;
+static __global__ void __launch_bounds__(256) stats_fold_kernel(const double* __restrict__ partial, int64_t nparts,
+                                                         double* __restrict__ out) {
+  __shared__ double sc[256], sm[256], s2[256];
+  const int row = blockIdx.y;
+  const double* pr = partial + (size_t)row * nparts * 3;
+  const int64_t lo = ((int64_t)blockIdx.x * 256 + threadIdx.x) * kFold;
+  Moments acc{0, 0, 0};
+  for (int j = 0; j < kFold; ++j) {
+    const int64_t b = lo + j;
+    if (b < nparts) acc = chan_merge(acc, Moments{pr[3 * b], pr[3 * b + 1], pr[3 * b + 2]});
+  }
+  sc[threadIdx.x] = acc.c; sm[threadIdx.x] = acc.mean; s2[threadIdx.x] = acc.m2;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      Moments r = chan_merge(Moments{sc[threadIdx.x], sm[threadIdx.x], s2[threadIdx.x]},
+                             Moments{sc[threadIdx.x + w], sm[threadIdx.x + w], s2[threadIdx.x + w]});
+      sc[threadIdx.x] = r.c; sm[threadIdx.x] = r.mean; s2[threadIdx.x] = r.m2;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = out + ((size_t)row * gridDim.x + blockIdx.x) * 3;
+    o[0] = sc[0]; o[1] = sm[0]; o[2] = s2[0];
+  }
 }
 
 // Cross-rank merge: gathered [R][rows][3] folded in rank order 0..R−1.

@@ -14,6 +14,7 @@
 #pragma once
 #include "common.cuh"
 #include "models.cuh"
+#include "stats.cuh"
 #include "vec2.cuh"
 
 namespace ens {
@@ -289,9 +290,35 @@ __device__ __forceinline__ void tsit5_save_bulk(const Args<T>& a, const bool (&l
 // uniform registers); 3 = as 2, full blocks stream their saves through shared
 // memory with bulk copies (dynamic shared memory 2·n·blockDim·W·sizeof(T);
 // the host checks the 16-byte alignment of every row).
-template <class M, class V, int SAVE>
+// Epilogue of the STATS instances, out of line so that it does not take part in
+// the register allocation of the step loop.
+template <int n, int W, class T>
+__device__ __noinline__ void fused_final_stats(const Args<T>& a, int64_t i0, const int64_t (&idx)[W],
+                                               const bool (&live)[W], const T (&yl)[n][W]) {
+  const int64_t nparts = cdiv_dev(a.N, 32 * W);
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#pragma unroll
+  for (int c = 0; c < n; ++c) {
+    double x[W];
+    bool use[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const bool valid = i0 + w < a.N, div0 = valid && !live[w];   // live is cleared only by a t0 divergence
+      x[w] = div0 ? (double)__ldg(a.u0 + (size_t)c * a.ld + idx[w]) : (double)yl[c][w];
+      use[w] = valid && isfinite(x[w]);
+    }
+    warp_stats_partial<W>(use, x, a.partial + ((size_t)c * nparts + wg) * 3);
+  }
+}
+
+// STATS (final state only): fused ensemble statistics of the stored final
+// states — one (count, mean, M2) partial per warp into a.partial
+// [n][cdiv(N, 32·W)][3], merged by stats_merge_kernel — so the states are not
+// read back (on a multi-GPU run they may live in another GPU's memory).
+template <class M, class V, int SAVE, bool STATS = false>
 __global__ void __launch_bounds__(256)
     tsit5_fixed_kernel(const Args<typename LaneOf<V>::T> a, const TsitCoef<typename CoefOf<V>::C> cf) {
+  static_assert(!STATS || SAVE == 0, "fused statistics are for final-state solves");
   using T = typename LaneOf<V>::T;
   using C = typename CoefOf<V>::C;
   constexpr int n = M::n, W = LaneOf<V>::W;
@@ -300,7 +327,11 @@ __global__ void __launch_bounds__(256)
   // bulk saves need every thread of the block at every barrier: full blocks only
   const bool bulk = (SAVE == 3) && (blk0 + (int64_t)blockDim.x * W <= a.N);
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
-  if (i0 >= a.N) return;
+  if (STATS) {   // the warp reduction needs every lane of a warp with any trajectory
+    if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * W >= a.N) return;
+  } else if (i0 >= a.N) {
+    return;
+  }
   int64_t idx[W];
   bool live[W];
 #pragma unroll
@@ -330,7 +361,9 @@ __global__ void __launch_bounds__(256)
   bool any = false;
 #pragma unroll
   for (int w = 0; w < W; ++w) any = any || live[w];
-  if (!any && !bulk) return;    // (in a bulk block a finished thread stays for the barriers, saving NaN)
+  // (in a bulk block a finished thread stays for the barriers, saving NaN; with
+  //  STATS it stays for the warp reduction)
+  if (!any && !bulk && !STATS) return;
   int nb = 0;                   // bulk saves issued by this block
   const V hdt = splat<V>(a.dt0);
   const HaParam<V, C> ha{cf.h};
@@ -358,6 +391,15 @@ __global__ void __launch_bounds__(256)
       else
         tsit5_save_coded<n, V, T, SAVE == 1>(a, idx, live, js, next, steps - 1, a.h_last, u, K, y);
     }
+  }
+  if constexpr (STATS) {   // statistics of the stored final states (u0 for lanes that diverged at t0)
+    T yl[n][W];
+#pragma unroll
+    for (int c = 0; c < n; ++c)
+#pragma unroll
+      for (int w = 0; w < W; ++w) yl[c][w] = lane(y[c], w);
+    fused_final_stats<n, W, T>(a, i0, idx, live, yl);
+    if (!any) return;
   }
   if (SAVE == 3 && bulk && threadIdx.x == 0) bulk_wait_all();
   if (SAVE) {
