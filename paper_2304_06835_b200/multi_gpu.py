@@ -168,8 +168,9 @@ def solve(model: str, alg: str, recipe: str, N_total: int, tspan, dt, *, dtype=t
     2. generate this shard's inputs on the rank's GPU from (input_seed, global index) — no scatter;
     3. solve the shard (global indices key the Philox noise, so every trajectory is bit-identical for
        any world size);
-    4. stats=True: per-rank (count, mean, M2) — fused in the EM kernels, a reduction pass over the
-       stored states otherwise — all-gathered and merged in fixed rank order on every rank;
+    4. stats=True: per-rank (count, mean, M2) — fused in the EM kernels and the fixed-step Tsit5
+       epilogue, a reduction pass over the stored states otherwise — all-gathered and merged in
+       fixed rank order on every rank;
     5. gather="peer": the solver stores straight into dst's [*lead, N_total] array (PeerGather; contiguous
        shards only); gather="nccl": NCCL gather of the rank blocks after the solve (equal N_r).
     `solve_kw` goes to ens.solve (adaptive, abstol, reltol, seed, refill, max_steps, ...)."""
@@ -206,14 +207,13 @@ def solve(model: str, alg: str, recipe: str, N_total: int, tspan, dt, *, dtype=t
                            n_accept=torch.empty(sh.n_local, dtype=torch.int32, device=dev),
                            n_reject=torch.empty(sh.n_local, dtype=torch.int32, device=dev),
                            stats=torch.empty((max(k, 1), n, 3), dtype=torch.float64, device=dev)
-                           if (stats and sde) else None)
-    sol = ens.solve(model, alg, u0, p, tspan, dt, saveat=saveat, stats=stats and sde, out=out,
+                           if stats else None)
+    # statistics come from the solve: fused into the EM kernels and the fixed-step Tsit5 epilogue,
+    # else a pass over the stored states run on this rank's GPU
+    sol = ens.solve(model, alg, u0, p, tspan, dt, saveat=saveat, stats=stats, out=out,
                     store_states=(gather is not None) or not (stats and sde),
                     index_offset=sh.index_offset, chunk_len=sh.chunk_len, chunk_stride=sh.chunk_stride, **solve_kw)
-    merged = None
-    if stats:
-        st = sol.stats if sde else ens.ensemble_stats(sol.u if k else sol.u.unsqueeze(0), device=dev)
-        merged = merge_stats(allgather_stats(st, group))
+    merged = merge_stats(allgather_stats(sol.stats, group)) if stats else None
     gathered = None
     if pg is not None:
         gathered = pg.complete()
