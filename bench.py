@@ -114,9 +114,15 @@ def cpu_baseline(N: int, nsteps_dt: float, sample: int, threads: int) -> dict:
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(work, chunks))
     wall = time.perf_counter() - t0
+    # one host core alone (SURVEY §8d reports single-core traj/s beside the all-core figure)
+    n1 = max(1, sample // (4 * threads))
+    t1 = time.perf_counter()
+    work(np.arange(n1))
+    wall1 = time.perf_counter() - t1
     return {"value": sample / wall, "unit": "trajectories/s", "cores": threads, "kind": "oracle",
             "sample": f"{sample} Lorenz Tsit5 fixed-dt fp32 trajectories (1000 steps each) spread over the "
-                      f"N={N} rho sweep; {threads} host threads; wall {wall:.2f} s"}
+                      f"N={N} rho sweep; {threads} host threads; wall {wall:.2f} s",
+            "single_core": {"value": n1 / wall1, "unit": "trajectories/s", "sample": f"first {n1} of the same sample"}}
 
 
 def load_traffic(tag: str):
