@@ -326,6 +326,7 @@ def main():
         del sol_a
         # NEXT-1: the same ρ sweep in fp64 at the north_star's tight tolerance, Tsit5 vs Vern9
         n_t = min(N, 10**6)
+        pk64 = torch.cuda.get_device_properties(dev).multi_processor_count * FP64_LANES_PER_SM * 2 * SM_MAX_MHZ * 1e6
         u0t, pt = ens.generate_inputs("lorenz", "rho_sweep", n_t, dtype=torch.float64, N_total=n_t, device=dev)
         for alg in ["tsit5", "vern9"]:
             sol_t = ens.solve("lorenz", alg, u0t, pt, tspan, dt, adaptive=True, abstol=1e-10, reltol=1e-10,
@@ -333,8 +334,11 @@ def main():
             mst = best_ms(lambda: ens.solve("lorenz", alg, u0t, pt, tspan, dt, adaptive=True, abstol=1e-10,
                                             reltol=1e-10, out=sol_t, stream=stream))
             att = int((sol_t.n_accept.to(torch.int64) + sol_t.n_reject.to(torch.int64)).sum().item())
+            fl = {"tsit5": 265.0, "vern9": 721.0}[alg]      # algorithmic FLOP per attempted Lorenz step
             also[f"{alg}_f64_tol1e-10_N{n_t}"] = {"trajectories_per_s": n_t / (mst / 1e3), "kernel_ms": mst,
-                                                  "attempted_steps_per_traj": att / n_t}
+                                                  "attempted_steps_per_traj": att / n_t,
+                                                  f"frac_fp64_peak_{fl:.0f}flop_per_attempt":
+                                                      att * fl / (mst / 1e3) / pk64}
         del u0t, pt, sol_t
         # NEXT-2: C3 (Robertson fp64, tol 1e-8, 100 save points) on Rosenbrock23 vs Rodas5
         n_s = min(N, 10**6)
@@ -346,8 +350,10 @@ def main():
             mss = best_ms(lambda: ens.solve("robertson", alg, ur, pr, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                                             reltol=1e-8, saveat=sa, out=sol_s, stream=stream))
             att = int((sol_s.n_accept.to(torch.int64) + sol_s.n_reject.to(torch.int64)).sum().item())
+            fl = {"rosenbrock23": 170.0, "rodas5": 600.0}[alg]   # ≈ FLOP per attempted Robertson step
             also[f"c3_{alg}_N{n_s}"] = {"trajectories_per_s": n_s / (mss / 1e3), "kernel_ms": mss,
-                                        "attempted_steps_per_traj": att / n_s}
+                                        "attempted_steps_per_traj": att / n_s,
+                                        f"frac_fp64_peak_{fl:.0f}flop_per_attempt": att * fl / (mss / 1e3) / pk64}
             del sol_s
         del ur, pr
 
