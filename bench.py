@@ -407,7 +407,7 @@ def main():
                                                                     if world > 1 else "")},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": load_traffic(tag),
-                         "kernel": f"tsit5_fixed_kernel<Lorenz,{'float' if args.dtype == 'f32' else 'double'}>",
+                         "kernel": f"tsit5_fixed_kernel<Lorenz,{'f2' if args.dtype == 'f32' else 'double'},SAVE=0,STATS>",
                          "kernel_ms": k_max, "flop_per_traj": flops_per_traj(nsteps),
                          "peak_basis": f"{props.multi_processor_count} SMs x {lanes} FMA lanes x 2 x {SM_MAX_MHZ:.0f} MHz",
                          "kernel_share_of_step": k_max / (ms_max / args.steps)},

@@ -291,11 +291,19 @@ __device__ __forceinline__ void tsit5_save_bulk(const Args<T>& a, const bool (&l
 // memory with bulk copies (dynamic shared memory 2·n·blockDim·W·sizeof(T);
 // the host checks the 16-byte alignment of every row).
 // Epilogue of the STATS instances, out of line so that it does not take part in
-// the register allocation of the step loop.
+// the register allocation of the step loop. Arguments are scalars and a small
+// aggregate by value: a reference to the kernel's Args (or to register arrays)
+// would force a per-thread copy into local memory (352 B, i.e. 1.7 GB of DRAM
+// writes per N = 10^7 launch).
+template <int n, int W, class T> struct FinalPack {
+  T y[n][W];
+  int64_t idx[W];
+  bool live[W];
+};
 template <int n, int W, class T>
-__device__ __noinline__ void fused_final_stats(const Args<T>& a, int64_t i0, const int64_t (&idx)[W],
-                                               const bool (&live)[W], const T (&yl)[n][W]) {
-  const int64_t nparts = cdiv_dev(a.N, 32 * W);
+__device__ __noinline__ void fused_final_stats(int64_t N, int64_t ld, const T* __restrict__ u0,
+                                               double* __restrict__ partial, int64_t i0, const FinalPack<n, W, T> fp) {
+  const int64_t nparts = cdiv_dev(N, 32 * W);
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 #pragma unroll
   for (int c = 0; c < n; ++c) {
@@ -303,11 +311,11 @@ __device__ __noinline__ void fused_final_stats(const Args<T>& a, int64_t i0, con
     bool use[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const bool valid = i0 + w < a.N, div0 = valid && !live[w];   // live is cleared only by a t0 divergence
-      x[w] = div0 ? (double)__ldg(a.u0 + (size_t)c * a.ld + idx[w]) : (double)yl[c][w];
+      const bool valid = i0 + w < N, div0 = valid && !fp.live[w];   // live is cleared only by a t0 divergence
+      x[w] = div0 ? (double)__ldg(u0 + (size_t)c * ld + fp.idx[w]) : (double)fp.y[c][w];
       use[w] = valid && isfinite(x[w]);
     }
-    warp_stats_partial<W>(use, x, a.partial + ((size_t)c * nparts + wg) * 3);
+    warp_stats_partial<W>(use, x, partial + ((size_t)c * nparts + wg) * 3);
   }
 }
 
@@ -393,12 +401,15 @@ __global__ void __launch_bounds__(256)
     }
   }
   if constexpr (STATS) {   // statistics of the stored final states (u0 for lanes that diverged at t0)
-    T yl[n][W];
+    FinalPack<n, W, T> fp;
 #pragma unroll
-    for (int c = 0; c < n; ++c)
+    for (int w = 0; w < W; ++w) {
+      fp.idx[w] = idx[w];
+      fp.live[w] = live[w];
 #pragma unroll
-      for (int w = 0; w < W; ++w) yl[c][w] = lane(y[c], w);
-    fused_final_stats<n, W, T>(a, i0, idx, live, yl);
+      for (int c = 0; c < n; ++c) fp.y[c][w] = lane(y[c], w);
+    }
+    fused_final_stats<n, W, T>(a.N, a.ld, a.u0, a.partial, i0, fp);
     if (!any) return;
   }
   if (SAVE == 3 && bulk && threadIdx.x == 0) bulk_wait_all();
