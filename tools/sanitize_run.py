@@ -22,6 +22,10 @@ for dt in [torch.float32, torch.float64]:
     u0, p = ens.generate_inputs("lorenz", "random10", N, dtype=dt, seed=1)
     sa = np.linspace(0, 1, 5)
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2)
+    ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, stats=True)          # fused statistics (fixed step)
+    ul, pl = ens.generate_inputs("lorenz", "random10", 600_001, dtype=dt, seed=2)  # > 8192 partials: fold + merge
+    ens.solve("lorenz", "tsit5", ul, pl, (0.0, 1.0), 0.25, stats=True)
+    del ul, pl
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, saveat=sa, stats=True)
     ub2, pb2 = ens.generate_inputs("lorenz", "random10", 1100, dtype=dt, seed=6)   # full blocks + a tail
     ens.solve("lorenz", "tsit5", ub2, pb2, (0.0, 1.0), 1e-2, saveat=np.arange(0, 101) * 1e-2)   # grid saves
