@@ -369,14 +369,14 @@ def main():
         rco = torch.empty(N, dtype=torch.int32, pin_memory=True)
         staging = None
         for _ in range(2):
-            _, _, staging = ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=16,
+            _, _, staging = ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=8,
                                            staging=staging, u_out_host=uo, retcode_host=rco)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=16, staging=staging,
+            ens.solve_host("lorenz", "tsit5", u0h, ph, tspan, dt, device=dev, n_chunks=8, staging=staging,
                            u_out_host=uo, retcode_host=rco)
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
@@ -384,7 +384,7 @@ def main():
         tsz = 4 if args.dtype == "f32" else 8
         e2e = {"value": N_total * args.steps / el.item(), "unit": "trajectories/s",
                "h2d_bytes_per_step": (3 + 3) * tsz * N, "d2h_bytes_per_step": 3 * tsz * N + 4 * N,
-               "api": "ensemble_solve_host (pinned host buffers, 16 chunks, H2D/compute/D2H overlapped, chunk solves on two streams)",
+               "api": "ensemble_solve_host (pinned host buffers, 8 ramped chunks, H2D/compute/D2H overlapped, chunk solves on two streams)",
                "per_rank_bytes": True}
 
     if rank == 0:

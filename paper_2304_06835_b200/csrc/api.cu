@@ -376,10 +376,22 @@ ens_status ensemble_solve_host(ens_model model, ens_alg alg, ens_dtype dtype, in
   cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
   cudaEventRecord(start, s);
   cudaStreamWaitEvent(sh, start, 0);
-  const int64_t base = N / C, rem = N % C;
+  // Chunk sizes: with 8+ chunks the first and last three ramp (weights 1, 2, 4 against 8 for the
+  // middle ones) so the copy-in of the first chunk and the copy-out of the last — the parts of the
+  // pipeline no compute overlaps — are small.
+  std::vector<int64_t> wgt(C, 8);
+  if (C >= 8 && N >= 1024 * 8 * C)   // (large N only: every chunk stays non-empty)
+    for (int j = 0; j < 3; ++j) wgt[j] = wgt[C - 1 - j] = (int64_t)1 << j;
+  int64_t wsum = 0;
+  for (int64_t c = 0; c < C; ++c) wsum += wgt[c];
+  std::vector<int64_t> bound(C + 1, 0);
+  for (int64_t c = 0, acc = 0; c < C; ++c) {
+    acc += wgt[c];
+    bound[c + 1] = (int64_t)((__int128)N * acc / wsum);
+  }
   int64_t lo = 0;
   for (int64_t c = 0; c < C && ok; ++c) {
-    const int64_t len = base + (c < rem ? 1 : 0);
+    const int64_t len = bound[c + 1] - bound[c];
     // H2D of chunk c (component rows are strided by N in the SoA layout)
     ok &= cudaMemcpy2DAsync((char*)d_u0 + lo * ts, N * ts, (const char*)u0_host + lo * ts, N * ts, len * ts, n,
                             cudaMemcpyHostToDevice, sh) == cudaSuccess;

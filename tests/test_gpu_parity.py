@@ -340,6 +340,28 @@ def test_solve_host_matches_device():
     np.testing.assert_array_equal(uh.numpy(), g[0])
 
 
+@pytest.mark.parametrize("n_chunks", [8, 16])
+def test_solve_host_ramped_chunks_match_device(n_chunks):
+    """Large N: ramped chunk sizes (1, 2, 4, 8, …, 8, 4, 2, 1) on two compute streams, fixed and
+    adaptive (static), fp32 and an SDE (index offsets per chunk key the Philox stream)."""
+    import torch
+
+    import paper_2304_06835_b200 as ens
+    N = 140_001
+    u0, p = make_inputs("lorenz", "random10", N, seed=5, dtype="f32")
+    U = torch.from_numpy(u0).pin_memory(); P = torch.from_numpy(p).pin_memory()
+    for kw in [{}, dict(adaptive=True, abstol=1e-6, reltol=1e-6)]:
+        uh, rch, _ = ens.solve_host("lorenz", "tsit5", U, P, (0.0, 1.0), 1e-3, n_chunks=n_chunks, **kw)
+        g, rc, *_ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, **kw)
+        np.testing.assert_array_equal(uh.numpy(), g[0])
+        np.testing.assert_array_equal(rch.numpy(), rc)
+    us, ps = make_inputs("lorenz_sde_add", "const", N, dtype="f32")
+    Us = torch.from_numpy(us).pin_memory(); Ps = torch.from_numpy(ps).pin_memory()
+    uh, rch, _ = ens.solve_host("lorenz_sde_add", "em", Us, Ps, (0.0, 0.1), 1e-3, n_chunks=n_chunks, seed=0xC4)
+    g, rc, *_ = gpu("lorenz_sde_add", "em", us, ps, (0.0, 0.1), 1e-3, seed=0xC4)
+    np.testing.assert_array_equal(uh.numpy(), g[0])
+
+
 # ------------------------------------------------------------ CRN (NEXT-3) --
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_crn_em_parity_and_stats(dtype):
