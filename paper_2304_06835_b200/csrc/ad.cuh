@@ -83,17 +83,17 @@ template <class M, class T>
 __device__ __forceinline__ void ad_jacobian(const T (&u)[M::n], const T (&p)[M::m], T t, T (&J)[M::n][M::n]) {
   constexpr int n = M::n, W = kAdPass<n>;
   static_assert(n % W == 0, "AD pass width must divide n");
-#pragma unroll (n <= 8 ? n / W : 1)
+#pragma unroll (n <= kUnrollMax ? n / W : 1)
   for (int k0 = 0; k0 < n; k0 += W) {
     Dual<T, W> y[n], o[n];
-#pragma unroll (n <= 8 ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : 1)
     for (int i = 0; i < n; ++i) {
       y[i].v = u[i];
 #pragma unroll
       for (int c = 0; c < W; ++c) y[i].d[c] = (i == k0 + c) ? T(1) : T(0);
     }
     M::f(y, p, t, o);
-#pragma unroll (n <= 8 ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : 1)
     for (int i = 0; i < n; ++i)
 #pragma unroll
       for (int c = 0; c < W; ++c) J[i][k0 + c] = o[i].d[c];
