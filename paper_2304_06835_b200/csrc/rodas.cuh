@@ -97,9 +97,9 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
   const T hg = h * T(Tab::gamma);
   const T ihg = T(1) / hg;
   const T ih = T(1) / h;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int i = 0; i < n; ++i)
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < n; ++j) W[i][j] = (i == j ? ihg : T(0)) - W[i][j];   // W = I/(hγ) − J
   int piv[n];
   T inv[n];
@@ -111,7 +111,7 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
     T hc[S - 1];
 #pragma unroll
     for (int j = 0; j < s; ++j) hc[j] = T(Tab::c(s, j)) * ih;                // c_sj / h
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int c = 0; c < n; ++c) {
       T acc = u[c];
 #pragma unroll
@@ -119,7 +119,7 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
       y[c] = acc;
     }
     M::f(y, par, t, F);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int c = 0; c < n; ++c) {
       T acc = F[c];
 #pragma unroll
@@ -128,7 +128,7 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
     }
     lu_solve<n, T>(W, piv, inv, r, K[s]);
   }
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int c = 0; c < n; ++c) un[c] = y[c] + K[S - 1][c];                    // u_new = Y_S + k_S
   return ok;
 }
@@ -138,7 +138,7 @@ template <int n, class T>
 __device__ __forceinline__ void rodas4_interp(T theta, const T (&u)[n], const T (&un)[n], const T (&K)[6][n],
                                               T (&o)[n]) {
   const T th1 = T(1) - theta;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int c = 0; c < n; ++c) {
     T s1 = T(rd_d(0, 0)) * K[0][c], s2 = T(rd_d(1, 0)) * K[0][c];
 #pragma unroll
@@ -203,7 +203,7 @@ template <class M, class T, bool SAVE> struct Rodas4Lane {
       const T tn = last ? a.tf : t + h;
       if (SAVE) rodas4_save<n, T>(a, i, js, t, tn, h, u, un, K);
       t = tn;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
       M::f(u, par, t, F0);
       ++nacc;
@@ -219,7 +219,7 @@ template <class M, class T, bool SAVE> struct Rodas4Lane {
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
     if (SAVE) {
       T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
       for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
     } else {
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) rodas4_fixed_kernel(const Args<T> a) {
       T un[n], K[6][n];
       if (!rodas_step<Rodas4Tab, M, T>(par, t, h, u, F0, un, K)) { ret = RET_SINGULAR; break; }
       if (SAVE) rodas4_save<n, T>(a, i, js, t, tn, h, u, un, K);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
       if (!last) M::f(u, par, tn, F0);
       ++nacc;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) rodas4_fixed_kernel(const Args<T> a) {
   }
   if (SAVE) {
     T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
     for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
   } else {
@@ -312,7 +312,7 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
     const T q2 = error_q2<n, T>(K[Tab::S - 1], u, un, a.abstol, a.reltol);
     if (q2 < T(1)) {
       t = clip ? target : t + h;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
       if (SAVE && clip && js < a.k) { store_point<n>(a, i, js, u); ++js; }
       M::f(u, par, t, F0);
@@ -329,7 +329,7 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
     if (SAVE) {
       T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
       for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
     } else {
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256) rodas_grid_fixed_kernel(const Args<T> a) 
       const T t = (T)(a.t0d + (double)s * a.dtd);
       T un[n], K[Tab::S][n];
       if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) { ret = RET_SINGULAR; break; }
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
       if (!last) M::f(u, par, (T)(a.t0d + (double)(s + 1) * a.dtd), F0);
       ++nacc;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(256) rodas_grid_fixed_kernel(const Args<T> a) 
   }
   if (SAVE) {
     T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
     for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
   } else {

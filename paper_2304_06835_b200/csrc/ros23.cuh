@@ -24,11 +24,11 @@ template <int n> constexpr bool kBranchSwap = (n > 4);
 template <int n, class T>
 __device__ __forceinline__ bool lu_factor(T (&A)[n][n], int (&piv)[n], T (&inv)[n]) {
   bool ok = true;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int kk = 0; kk < n; ++kk) {
     int pr = kk;
     T best = absT(A[kk][kk]);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int i = kk + 1; i < n; ++i) {
       const T v = absT(A[i][kk]);
       if (v > best) { best = v; pr = i; }
@@ -40,10 +40,10 @@ __device__ __forceinline__ bool lu_factor(T (&A)[n][n], int (&piv)[n], T (&inv)[
     // POLLU 12–26 % faster). For n ≤ 4 plain selects measured faster (OREGO,
     // refill Rosenbrock23 on C3: 5–10 %).
     if (!kBranchSwap<n> || pr != kk) {
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int i = kk + 1; i < n; ++i) {
         const bool sw = (pr == i);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
         for (int j = 0; j < n; ++j) {
           const T a0 = A[kk][j], a1 = A[i][j];
           A[kk][j] = sw ? a1 : a0;
@@ -54,11 +54,11 @@ __device__ __forceinline__ bool lu_factor(T (&A)[n][n], int (&piv)[n], T (&inv)[
     const T pivot = A[kk][kk];
     ok = ok && (pivot != T(0)) && finiteT(pivot);
     inv[kk] = T(1) / pivot;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int i = kk + 1; i < n; ++i) {
       const T l = A[i][kk] * inv[kk];
       A[i][kk] = l;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = kk + 1; j < n; ++j) A[i][j] = fmaT(-l, A[kk][j], A[i][j]);
     }
   }
@@ -69,12 +69,12 @@ template <int n, class T>
 __device__ __forceinline__ void lu_solve(const T (&LU)[n][n], const int (&piv)[n], const T (&inv)[n], const T (&b)[n],
                                          T (&x)[n]) {
   T z[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int i = 0; i < n; ++i) z[i] = b[i];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int kk = 0; kk < n; ++kk) {
     if (!kBranchSwap<n> || piv[kk] != kk) {   // branch for n > 4, as in lu_factor
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int i = kk + 1; i < n; ++i) {
         const bool sw = (piv[kk] == i);
         const T z0 = z[kk], z1 = z[i];
@@ -83,17 +83,17 @@ __device__ __forceinline__ void lu_solve(const T (&LU)[n][n], const int (&piv)[n
       }
     }
   }
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int i = 0; i < n; ++i) {          // forward, unit lower
     T s = z[i];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < i; ++j) s = fmaT(-LU[i][j], z[j], s);
     z[i] = s;
   }
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int i = n - 1; i >= 0; --i) {     // backward
     T s = z[i];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = i + 1; j < n; ++j) s = fmaT(-LU[i][j], x[j], s);
     x[i] = s * inv[i];
   }
@@ -109,9 +109,9 @@ __device__ __forceinline__ bool ros23_step(const T (&par)[M::m], T t, T h, const
   T W[n][n];
   model_jacobian<M, T>(u, par, t, W);          // J (hand-written or forward-mode AD)
   const T hd = h * d;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int i = 0; i < n; ++i)
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < n; ++j) W[i][j] = (i == j ? T(1) : T(0)) - hd * W[i][j];   // W = I − h d J
   int piv[n];
   T inv[n];
@@ -119,25 +119,25 @@ __device__ __forceinline__ bool ros23_step(const T (&par)[M::m], T t, T h, const
   lu_solve<n, T>(W, piv, inv, F0, k1);        // k1 = W⁻¹ F0
   T y[n], F1[n], r[n], k3[n];
   const T hh = h * T(0.5);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) y[j] = fmaT(hh, k1[j], u[j]);
   M::f(y, par, t + hh, F1);                  // F1 = f(u + h/2 k1)
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) r[j] = F1[j] - k1[j];
   lu_solve<n, T>(W, piv, inv, r, k2);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) k2[j] = k2[j] + k1[j];   // k2 = W⁻¹(F1 − k1) + k1
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) un[j] = fmaT(h, k2[j], u[j]);
   M::f(un, par, t + h, F2);                  // F2 = f(u_new)
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) {
     const T aa = fmaT(-e32, k2[j] - F1[j], F2[j]);
     r[j] = fmaT(T(-2), k1[j] - F0[j], aa);   // F2 − e32(k2 − F1) − 2(k1 − F0)
   }
   lu_solve<n, T>(W, piv, inv, r, k3);
   const T h6 = h * T(1.0 / 6.0);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) E[j] = h6 * (fmaT(T(-2), k2[j], k1[j]) + k3[j]);   // E = h/6 (k1 − 2k2 + k3)
   return ok;
 }
@@ -148,7 +148,7 @@ __device__ __forceinline__ void ros23_interp(T theta, T h, const T (&u)[n], cons
   const T d = T(r23_d()), inv12d = T(r23_inv12d());
   const T c1 = (theta * (T(1) - theta)) * inv12d;
   const T c2 = (theta * (theta - T(2) * d)) * inv12d;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int j = 0; j < n; ++j) o[j] = fmaT(h, fmaT(c2, k2[j], c1 * k1[j]), u[j]);
 }
 
@@ -204,7 +204,7 @@ template <class M, class T, bool SAVE> struct Ros23Lane {
       const T tn = last ? a.tf : t + h;
       if (SAVE) ros23_save<n, T>(a, i, js, t, tn, h, u, k1, k2, un);
       t = tn;
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) { u[j] = un[j]; F0[j] = F2[j]; }
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, 7.0 / 20.0, 2.0 / 10.0);
@@ -219,7 +219,7 @@ template <class M, class T, bool SAVE> struct Ros23Lane {
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
     if (SAVE) {
       T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
       for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
     } else {
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) ros23_fixed_kernel(const Args<T> a) {
       T un[n], F2[n], k1[n], k2[n], E[n];
       if (!ros23_step<M, T>(par, t, h, u, F0, un, F2, k1, k2, E)) { ret = RET_SINGULAR; break; }
       if (SAVE) ros23_save<n, T>(a, i, js, t, last ? a.tf : (T)(a.t0d + (double)(s + 1) * a.dtd), h, u, k1, k2, un);
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) { u[j] = un[j]; F0[j] = F2[j]; }
       ++nacc;
     }
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) ros23_fixed_kernel(const Args<T> a) {
   }
   if (SAVE) {
     T nanv[n];
-#pragma unroll (n <= kUnrollMax ? n : 1)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
     for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
     for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
   } else {
