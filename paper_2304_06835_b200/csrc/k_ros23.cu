@@ -22,7 +22,9 @@ ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       const char* e = getenv("ENS_TUNE_ROS23_MINB");
       return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
     }();
-    if (minb == 3 && M::n <= 4 && !opt->refill) {
+    // (only when the ensemble fills more than two blocks per SM: a small ensemble — the stiff suite's
+    //  8192 — gains no residency from the cap and pays for its spills, OREGO 9 % slower)
+    if (minb == 3 && M::n <= 4 && !opt->refill && a.N > (int64_t)sm_count() * 2 * 256) {
       if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
       else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
     } else {
