@@ -15,7 +15,12 @@ ens_status run_sde(int alg, const Args<T>& a, const ens_options* opt, cudaStream
       return ENS_E_UNSUPPORTED;
     }
   } else {
-    if constexpr (sizeof(T) == 8 && M::nw > 3) {   // fp64 CRN: three blocks per SM (em_kernel_b3)
+    // register caps only pay when the ensemble fills the SMs beyond two blocks each (cf. k_ros23.cu)
+    const bool large = a.N > (int64_t)sm_count() * 2 * 256;
+    if (!large) {
+      if (opt->want_stats) em_kernel<M, T, true><<<g, b, 0, s>>>(a);
+      else em_kernel<M, T, false><<<g, b, 0, s>>>(a);
+    } else if constexpr (sizeof(T) == 8 && M::nw > 3) {   // fp64 CRN: three blocks per SM (em_kernel_b3)
       if (opt->want_stats) em_kernel_b3<M, T, true><<<g, b, 0, s>>>(a);
       else em_kernel_b3<M, T, false><<<g, b, 0, s>>>(a);
     } else if constexpr (sizeof(T) == 4 && M::nw == 3) {   // fp32 C4: four blocks per SM (72 -> 64 regs, 1-3 %)
