@@ -1,39 +1,10 @@
 // k_ros23.cu — Rosenbrock23 kernel instances (fixed step; adaptive static or
 // refill) for the ODE models without events.
-#include <cstdlib>
+#include <type_traits>
 
-#include "launch.cuh"
-#include "ros23.cuh"
+#include "ros23_launch.cuh"
 
 namespace ens {
-
-template <class M, class T>
-ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
-  const bool save = a.k > 0;
-  if (!opt->adaptive) {
-    if (save) launch_fixed(ros23_fixed_kernel<M, T, true>, a, s);
-    else launch_fixed(ros23_fixed_kernel<M, T, false>, a, s);
-  } else {
-    // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
-    // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log) — for small systems
-    // only: HIRES (n = 8) spills under the cap and runs 17 % slower (profiles/ros23_minb_models_r01.log).
-    // A cap of 4 blocks (64 regs) spills on C3 as well and is slower. ENS_TUNE_ROS23_MINB=1 reverts.
-    static const int minb = [] {
-      const char* e = getenv("ENS_TUNE_ROS23_MINB");
-      return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
-    }();
-    // (only when the ensemble fills more than two blocks per SM: a small ensemble — the stiff suite's
-    //  8192 — gains no residency from the cap and pays for its spills, OREGO 9 % slower)
-    if (minb == 3 && M::n <= 4 && !opt->refill && a.N > (int64_t)sm_count() * 2 * 256) {
-      if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
-      else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
-    } else {
-      if (save) launch_adaptive<Ros23Lane<M, T, true>, T>(a, opt->refill, s);
-      else launch_adaptive<Ros23Lane<M, T, false>, T>(a, opt->refill, s);
-    }
-  }
-  return launch_status();
-}
 
 template <class T>
 ens_status launch_ros23(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s) {
@@ -41,6 +12,7 @@ ens_status launch_ros23(int model, const Args<T>& a, const ens_options* opt, cud
     using M = decltype(mt);
     if constexpr (HasEvent<M>::value) return ENS_E_UNSUPPORTED;                  // events: Tsit5 only (R18)
     else if constexpr (M::n > 8 && sizeof(T) == 4) return ENS_E_UNSUPPORTED;     // POLLU: fp64 only
+    else if constexpr (std::is_same<M, Pollu>::value) return run_ros23_pollu(a, opt, s);   // k_ros23_pollu.cu
     else return run_ros23<M, T>(a, opt, s);
   });
 }
