@@ -1,6 +1,6 @@
 // launch.cuh — launch configuration shared by the per-algorithm translation
-// units (k_tsit5.cu, k_vern7.cu, k_vern9.cu, k_ros23.cu, k_rodas4.cu, k_rodas5.cu, k_sde.cu) and the ABI
-// (api.cu).
+// units (k_tsit5.cu, k_vern7.cu, k_vern9.cu, k_ros23.cu, k_rodas4.cu, k_rodas5.cu, k_sde.cu, and the
+// POLLU units k_ros23_pollu.cu, k_rodas4_pollu.cu, k_rodas5_pollu.cu) and the ABI (api.cu).
 // Each algorithm's kernel instances live in their own .cu so the library
 // builds in parallel; api.cu only sees the launch_* entry points below.
 #pragma once
