@@ -74,6 +74,9 @@ def lib() -> ctypes.CDLL:
         L.orc_normals.argtypes = [i32, u64, u64, i64, i64, i32, vp]
         L.orc_fixed_grid.argtypes = [dbl, dbl, dbl, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
         L.orc_lu_solve.argtypes = [i32, i32, vp, vp, vp]
+        L.orc_set_plain.argtypes = [i32]
+        L.orc_set_plain.restype = i32
+        L.orc_ros23_step.argtypes = [i32, vp, dbl, dbl, vp, vp, vp]
         L.orc_solve.argtypes = [i32, i32, i32, i64, vp, vp, i32, vp, dbl, dbl, dbl, i32, dbl, dbl, i64, u64,
                                 vp, i32, vp, vp, vp, vp]
         L.orc_stats.argtypes = [i32, i64, i32, i32, vp, vp, vp, vp, ctypes.POINTER(i64)]
@@ -209,6 +212,35 @@ def normals(seed: int, gidx: int, step0: int, count: int, dtype="f64", nw: int =
     out = np.zeros((count, nw), NP_DTYPE[dtype])
     lib().orc_normals(DTYPES[dtype], seed, gidx, step0, count, nw, _p(out))
     return out
+
+
+def set_plain(on: bool) -> bool:
+    """Test-only: evaluate the PI controller literally with libm pow and
+    Box–Muller with libm log/sin/cos (True), or in the canonical forms of
+    DESIGN R2 / R8 that the kernels follow (False, the default). Returns the
+    previous mode."""
+    return bool(lib().orc_set_plain(int(bool(on))))
+
+
+class plain_mode:
+    """Context manager: ``with oracle.plain_mode(): ...`` runs the oracle in plain mode."""
+
+    def __enter__(self):
+        self._prev = set_plain(True)
+        return self
+
+    def __exit__(self, *exc):
+        set_plain(self._prev)
+        return False
+
+
+def ros23_step(model: str, u, p, t: float, h: float):
+    """One fp64 Rosenbrock23 step from u (F0 = f(u)): (u_new, E), or None if W is singular."""
+    u = np.ascontiguousarray(u, np.float64); p = np.ascontiguousarray(p, np.float64)
+    un = np.zeros_like(u); E = np.zeros_like(u)
+    if lib().orc_ros23_step(MODELS[model], _p(p), float(t), float(h), _p(u), _p(un), _p(E)):
+        return None
+    return un, E
 
 
 def fixed_grid(t0, tf, dt):

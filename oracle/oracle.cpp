@@ -22,8 +22,14 @@
 // invariants, Philox known-answer vectors, the noise-stream structure, exact
 // discrete EM / SIEA moments for GBM, one-step SDE increment moments, LU vs
 // Cramer, model values/Jacobians vs finite differences, stats on exact cases.
+// Rosenbrock23's embedded estimate E is pinned against the true local error
+// (closed form e^z and a DOP853 reference step, tests/test_oracle_readings.py).
 // Parity unpinned (oracle-vs-GPU only): the PI-controller
-// constants (R2) — the paper does not print them.
+// constants (R2) — the paper does not print them — and the scale of Vern7's
+// error estimate (R21: one typed literature constant; every order condition
+// holds for any scale).
+// Plain mode (orc_set_plain, tests only): the controller as printed with libm
+// pow and Box–Muller with libm log/sin/cos, to measure what readings R2 / R8 change.
 // =============================================================================
 #include <cmath>
 #include <cstdint>
@@ -65,6 +71,14 @@ static bool dims(int model, Dims* d) {
 
 template <class T> static T log2_spec(T x);
 template <class T> static T exp2_spec(T z);
+
+// "Plain" mode (test-only cross-check of readings R2 and R8, set by
+// orc_set_plain): the PI controller is evaluated literally as printed at P:120
+// with libm pow on q = sqrt(q²), and Box–Muller with libm
+// log / sqrt / sin / cos. Default 0 = the canonical exponent-domain / polynomial
+// forms that the kernels follow. The test suite runs both modes on
+// the same ensembles to measure what the readings change (DESIGN R2, R8).
+static int g_plain = 0;
 
 // Hill power x^e for the CRN model (DESIGN R14): 2^{e·L(x)} with the
 // polynomial log2 / exp2 of R2, x clamped to [1e-30, 1e30], exponent to ±120.
@@ -441,13 +455,25 @@ static void call_words(uint64_t seed, uint64_t gidx, uint64_t c, uint32_t w[4]) 
   philox4x32_10(ctr, key, w);
 }
 template <class T> static void call_normals(uint64_t seed, uint64_t gidx, uint64_t c, T* zc);
+// Plain Box–Muller (P:157 N(0,1) draws; g_plain = 1): R = sqrt(−2 ln U_a),
+// (sin, cos)(2π U_b), every operation in T with libm.
+template <class T> static void bm_plain(T Ua, T Ub, T* R, T* sn, T* cs) {
+  *R = std::sqrt(T(-2) * std::log(Ua));
+  const T th = (T)6.283185307179586476925286766559 * Ub;
+  *sn = std::sin(th);
+  *cs = std::cos(th);
+}
+
 template <> void call_normals<float>(uint64_t seed, uint64_t gidx, uint64_t c, float* zc) {
   uint32_t w[4]; call_words(seed, gidx, c, w);
   float U[4]; for (int i = 0; i < 4; ++i) U[i] = u01_f32(w[i]);
   for (int q = 0; q < 2; ++q) {
-    float sn, cs;
-    const float R = bm_radius<float>(U[2 * q]);
-    sincospi_spec<float>(2.0f * U[2 * q + 1], &sn, &cs);
+    float sn, cs, R;
+    if (g_plain) bm_plain<float>(U[2 * q], U[2 * q + 1], &R, &sn, &cs);
+    else {
+      R = bm_radius<float>(U[2 * q]);
+      sincospi_spec<float>(2.0f * U[2 * q + 1], &sn, &cs);
+    }
     zc[2 * q] = R * cs;
     zc[2 * q + 1] = R * sn;
   }
@@ -455,9 +481,12 @@ template <> void call_normals<float>(uint64_t seed, uint64_t gidx, uint64_t c, f
 template <> void call_normals<double>(uint64_t seed, uint64_t gidx, uint64_t c, double* zc) {
   uint32_t w[4]; call_words(seed, gidx, c, w);
   const double Ua = u01_f64(w[0], w[1]), Ub = u01_f64(w[2], w[3]);
-  double sn, cs;
-  const double R = bm_radius<double>(Ua);
-  sincospi_spec<double>(2.0 * Ub, &sn, &cs);
+  double sn, cs, R;
+  if (g_plain) bm_plain<double>(Ua, Ub, &R, &sn, &cs);
+  else {
+    R = bm_radius<double>(Ua);
+    sincospi_spec<double>(2.0 * Ub, &sn, &cs);
+  }
   zc[0] = R * cs;
   zc[1] = R * sn;
 }
@@ -607,7 +636,32 @@ template <class T> static T half_log2_q(T q2) {
   const T x = std::fmin(std::fmax(q2, (T)1e-30), (T)1e30);
   return T(0.5) * log2_spec<T>(x);
 }
+// Plain mode (g_plain = 1): the same controller written literally:
+// q = sqrt(q²); accept iff q < 1; accept: q == 0 → h·qmax, else
+// qq = clamp(pow(q, β1) / pow(q_old, β2) / η, 1/qmax, 1/qmin), h_new = h / qq,
+// q_old ← max(q, 1e-4); reject: h_new = h / min(1/qmin, pow(q, β1) / η).
+// *lq_old then holds q_old itself (initialised by ctrl_init).
+template <class T> static T ctrl_init() { return g_plain ? (T)1e-4 : (T)L_FLOOR; }
+template <class T> static bool accept_q(T q2) { return g_plain ? std::sqrt(q2) < T(1) : q2 < T(1); }
+template <class T> static T pi_accept_plain(const Ctrl& C, T h, T q2, T* q_old) {
+  const T q = std::sqrt(q2);
+  T hn;
+  if (q == T(0)) hn = h / (T)C.qmax_inv;
+  else {
+    T qq = std::pow(q, (T)C.beta1) / std::pow(*q_old, (T)C.beta2);
+    qq = std::fmax((T)C.qmax_inv, std::fmin((T)C.qmin_inv, qq / (T)C.eta));
+    hn = h / qq;
+  }
+  *q_old = std::fmax(q, (T)C.qold_floor);
+  return hn;
+}
+template <class T> static T pi_reject_plain(const Ctrl& C, T h, T q2) {
+  const T q = std::sqrt(q2);
+  return h / std::fmin((T)C.qmin_inv, std::pow(q, (T)C.beta1) / (T)C.eta);
+}
+
 template <class T> static T pi_accept(const Ctrl& C, T h, T q2, T* lq_old) {
+  if (g_plain) return pi_accept_plain<T>(C, h, q2, lq_old);
   const T lq = half_log2_q<T>(q2);
   T z = std::fma((T)C.beta1, lq, (T)C_ETA);
   z = std::fma(-(T)C.beta2, *lq_old, z);
@@ -616,6 +670,7 @@ template <class T> static T pi_accept(const Ctrl& C, T h, T q2, T* lq_old) {
   return h * exp2_spec<T>(-z);
 }
 template <class T> static T pi_reject(const Ctrl& C, T h, T q2) {
+  if (g_plain) return pi_reject_plain<T>(C, h, q2);
   const T lq = half_log2_q<T>(q2);
   const T z = std::fmin((T)Z_MAX, std::fma((T)C.beta1, lq, (T)C_ETA));
   return h * exp2_spec<T>(-z);
@@ -664,7 +719,7 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
     const Ctrl& C = CTRL_TSIT5;
     const T abstol = (T)o.abstol, reltol = (T)o.reltol;
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T lq_old = (T)L_FLOOR;
+    T lq_old = ctrl_init<T>();
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -673,7 +728,7 @@ static void solve_tsit5(const Opts& o, Traj<T>& tr) {
       tsit5_step<T>(model, n, p, t, h, u, K, unew, E);
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
-      if (q2 < T(1)) {                              // accept iff q < 1
+      if (accept_q<T>(q2)) {                            // accept iff q < 1
         T tn = last ? tf : t + h;
         // Event (DESIGN R18): downward zero crossing of the condition
         // inside the accepted step → locate it on the step's interpolant by a
@@ -871,7 +926,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
     if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
   } else {
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T lq_old = (T)L_FLOOR;
+    T lq_old = ctrl_init<T>();
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -885,7 +940,7 @@ static void solve_ros23(const Opts& o, Traj<T>& tr) {
         continue;
       }
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
-      if (q2 < T(1)) {
+      if (accept_q<T>(q2)) {
         const T tn = last ? tf : t + h;
         while (js < k && tau[js] <= tn) {
           if (tau[js] == tn) put(tr.save, n, js, unew);
@@ -1031,7 +1086,7 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
     if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
   } else {
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T lq_old = (T)L_FLOOR;
+    T lq_old = ctrl_init<T>();
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -1045,7 +1100,7 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
         continue;
       }
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
-      if (q2 < T(1)) {
+      if (accept_q<T>(q2)) {
         const T tn = last ? tf : t + h;
         save_in_step(t, tn, h);
         t = tn;
@@ -1167,7 +1222,7 @@ static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
     if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
   } else {
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T lq_old = (T)L_FLOOR;
+    T lq_old = ctrl_init<T>();
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -1182,7 +1237,7 @@ static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
         continue;
       }
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
-      if (q2 < T(1)) {
+      if (accept_q<T>(q2)) {
         t = clip ? target : t + h;
         for (int j = 0; j < n; ++j) u[j] = unew[j];
         if (clip && js < k) { put(tr.save, n, js, u); ++js; }
@@ -1361,7 +1416,7 @@ static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const in
     const Ctrl& C = *tb.ctrl;
     const T abstol = (T)o.abstol, reltol = (T)o.reltol;
     T h = (T)std::min(o.dt, o.tf - o.t0);
-    T lq_old = (T)L_FLOOR;
+    T lq_old = ctrl_init<T>();
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
@@ -1371,7 +1426,7 @@ static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const in
       verner_step<T>(tb, model, n, p, t, h, u, K, unew, E);
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
-      if (q2 < T(1)) {
+      if (accept_q<T>(q2)) {
         t = clip ? target : t + h;
         for (int j = 0; j < n; ++j) u[j] = unew[j];
         if (clip && js < k) { put(tr.save, n, js, u); ++js; }
@@ -1646,6 +1701,19 @@ void orc_normals(int dtype, uint64_t seed, uint64_t gidx, int64_t step0, int64_t
     if (dtype == 0) orc::normalsN<float>(sf, (uint64_t)(step0 + s), nw, (float*)out + nw * s);
     else orc::normalsN<double>(sd, (uint64_t)(step0 + s), nw, (double*)out + nw * s);
   }
+}
+
+// Test-only switch of the R2 / R8 evaluation forms (see g_plain). Returns the previous mode.
+int orc_set_plain(int on) { const int prev = orc::g_plain; orc::g_plain = on ? 1 : 0; return prev; }
+
+// One Rosenbrock23 step (fp64) from (t, u, h) with F0 = f(u): u_new and the
+// embedded estimate E (pins of the error estimate). Returns 1 if W is singular.
+int orc_ros23_step(int model, const double* p, double t, double h, const double* u, double* unew, double* E) {
+  orc::Dims d;
+  if (!orc::dims(model, &d)) return 2;
+  double F0[orc::NMAX], F2[orc::NMAX], k1[orc::NMAX], k2[orc::NMAX];
+  orc::rhs<double>(model, u, p, t, F0);
+  return orc::ros23_step<double>(model, d.n, p, t, h, u, F0, unew, F2, k1, k2, E) ? 0 : 1;
 }
 
 void orc_fixed_grid(double t0, double tf, double dt, int64_t* nsteps, double* h_last) {

@@ -99,10 +99,30 @@ def test_tsit5_expdecay_closed_form():
     assert abs(_R_tsit5(-0.1, 1 / 720) ** 10 - v) > 1e-13
     # several λ, h (vectorised over trajectories) in fp64 and fp32
     lam = np.array([0.5, 1.0, 3.0, 7.5])
-    for dtype, tol in [("f64", 1e-13), ("f32", 1e-5)]:   # fp32: 40 steps × a few ulp
-        out, rc, na, _ = oracle.solve("expdecay", "tsit5", np.ones((1, 4)), lam[None, :], (0, 2), 0.05, dtype=dtype)
-        expect = _R_tsit5(-lam * 0.05, g6) ** 40
-        np.testing.assert_allclose(out[0, 0].astype(np.float64), expect, rtol=tol)
+    out, rc, na, _ = oracle.solve("expdecay", "tsit5", np.ones((1, 4)), lam[None, :], (0, 2), 0.05, dtype="f64")
+    np.testing.assert_allclose(out[0, 0], _R_tsit5(-lam * 0.05, g6) ** 40, rtol=1e-13)
+    # fp32 (R1): the products h·a_ij are rounded to fp32, which perturbs the
+    # stability polynomial itself (4.8e-6 after 40 steps at λ = 7.5). The exact
+    # expectation is R̃(z)^40 with R̃ built from the fp32-rounded h·a_ij (stage
+    # recursion evaluated in fp64); what remains is arithmetic rounding, bounded
+    # by one fp32 unit roundoff (2^-24) per step: 40·2^-24 = 2.4e-6.
+    c, A, bt, r = oracle.tsit5_tableau()
+    out, *_ = oracle.solve("expdecay", "tsit5", np.ones((1, 4)), lam[None, :], (0, 2), 0.05, dtype="f32")
+    h32 = np.float32(0.05)
+    ha = (h32 * A.astype(np.float32)).astype(np.float64)     # h·a_ij rounded to fp32 (R1)
+    for i, l in enumerate(lam):
+        l32 = float(np.float32(l))
+        u = 1.0
+        for _ in range(40):
+            K = [-l32 * u]
+            for s in range(1, 7):
+                y = u + sum(ha[s, j] * K[j] for j in range(s))
+                K.append(-l32 * y)
+            u = y
+        assert abs(float(out[0, 0, i]) - u) <= 40 * 2.0**-24 * abs(u), (l, float(out[0, 0, i]), u)
+        # and the rounded-coefficient polynomial is what separates fp32 from R(z)^40
+        exact = _R_tsit5(-l * 0.05, g6) ** 40
+        assert abs(float(out[0, 0, i]) - exact) <= abs(u - exact) + 40 * 2.0**-24 * abs(u)
 
 
 def test_tsit5_harmonic_closed_form():
