@@ -124,6 +124,11 @@ typedef struct {
                               0 -> N. Lets a shard write its states straight into a slice of a larger
                               [k][n][out_ld] array — e.g. another GPU's gather buffer mapped through CUDA
                               IPC (the fused gather of multi_gpu.PeerGather). ensemble_solve_host: must be 0. */
+  int32_t bulk_saves;      /* 1: fixed-step Tsit5 grid saves staged through shared memory and written
+                              row-wise with cp.async.bulk (needs a 16-B aligned u_out and out_ld·sizeof(T)
+                              a multiple of 16, else ignored); bit-identical to the default 0 (per-thread
+                              stores), which measured faster (DESIGN §5 "Saveat-dense"). No other tuning
+                              state exists: the library reads no environment variables. */
 } ens_options;
 
 typedef struct {

@@ -39,7 +39,7 @@ class _Options(ctypes.Structure):
                 ("max_steps", ctypes.c_int64), ("seed", ctypes.c_uint64), ("saveat", ctypes.c_void_p),
                 ("n_saveat", ctypes.c_int32), ("p_broadcast", ctypes.c_int32), ("want_stats", ctypes.c_int32),
                 ("refill", ctypes.c_int32), ("index_offset", ctypes.c_int64), ("chunk_len", ctypes.c_int64),
-                ("chunk_stride", ctypes.c_int64), ("out_ld", ctypes.c_int64)]
+                ("chunk_stride", ctypes.c_int64), ("out_ld", ctypes.c_int64), ("bulk_saves", ctypes.c_int32)]
 
 
 class _Output(ctypes.Structure):
@@ -163,7 +163,7 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
           adaptive: bool = False, abstol: float = 1e-6, reltol: float = 1e-3, saveat: Optional[Sequence[float]] = None,
           max_steps: int = 0, seed: int = 0, stats: bool = False, refill: bool = False, index_offset: int = 0,
           chunk_len: int = 0, chunk_stride: int = 0, store_states: bool = True, workspace: Optional[Workspace] = None,
-          out: Optional[Solution] = None, stream=None) -> Solution:
+          out: Optional[Solution] = None, stream=None, bulk_saves: bool = False) -> Solution:
     """ensemble_solve on device tensors. u0 [n, N], p [m, N] (or [m]: broadcast), same float dtype."""
     import numpy as np
     if not u0.is_cuda or not p.is_cuda:
@@ -180,6 +180,7 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
     k = 0 if sa is None else sa.size
     opt = _options(adaptive, abstol, reltol, max_steps, seed, sa, p_broadcast, stats, refill, index_offset,
                    chunk_len, chunk_stride)
+    opt.bulk_saves = int(bool(bulk_saves))
     dev = u0.device
     if out is None:
         shape = (k, n, N) if k else (n, N)
@@ -210,6 +211,13 @@ def solve(model: str, alg: str, u0: torch.Tensor, p: torch.Tensor, tspan: Sequen
                               float(tspan[1]), float(dt), ctypes.byref(opt), ctypes.byref(o), _stream_ptr(stream))
     if st:
         raise EnsError(st, "ensemble_solve")
+    if stream is not None and stream != torch.cuda.current_stream(dev):
+        # the kernel runs on `stream`: keep the caching allocator from handing this call's
+        # temporaries (workspace, contiguous copies of u0 / p, outputs) to other work on the
+        # current stream before the kernel is done with them
+        for t in (u0, p, ws, out.u, out.retcode, out.n_accept, out.n_reject, out.stats):
+            if t is not None and t.is_cuda and t.device == dev:
+                t.record_stream(stream)
     return out
 
 

@@ -267,8 +267,8 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   if (opt->want_stats) {
     const bool fused = fused_stats(alg, opt);
     if (!is_sde_alg(alg) && !fused) {
-      const dim3 g((unsigned)L.nparts, (unsigned)L.rows);
-      stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, a.ldo, kStatsChunk, a.partial);
+      const dim3 g((unsigned)L.nparts, (unsigned)std::min(L.rows, kMaxGridY));
+      stats_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)out->u_out, N, a.ldo, kStatsChunk, a.partial, L.rows);
     }
     // EM: one partial per block; fused Tsit5: one per warp (two trajectories per lane in fp32)
     const int64_t nparts = is_sde_alg(alg) ? (int64_t)grid_for(N).x
@@ -276,7 +276,8 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
     if (nparts > 4 * 256 * kFold) {   // many partials (fused per-warp stats): fold in parallel first
       double* p2 = (double*)(ws + L.partial2);
       const int64_t nblk = cdiv(nparts, 256 * kFold);
-      stats_fold_kernel<<<dim3((unsigned)nblk, (unsigned)L.rows), 256, 0, s>>>(a.partial, nparts, p2);
+      stats_fold_kernel<<<dim3((unsigned)nblk, (unsigned)std::min(L.rows, kMaxGridY)), 256, 0, s>>>(a.partial, nparts,
+                                                                                                   p2, L.rows);
       stats_merge_kernel<<<L.rows, 256, 0, s>>>(p2, (int)nblk, out->stats);
     } else {
       stats_merge_kernel<<<L.rows, 256, 0, s>>>(a.partial, (int)nparts, out->stats);
@@ -511,10 +512,11 @@ ens_status ens_ensemble_stats(ens_dtype dtype, const void* x, int64_t N, int64_t
   if (!workspace || workspace_bytes < ens_stats_workspace_bytes(N, rows)) return ENS_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t nparts = cdiv(N, kStatsChunk);
-  const dim3 g((unsigned)nparts, (unsigned)rows);
+  const dim3 g((unsigned)nparts, (unsigned)std::min(rows, kMaxGridY));
   double* part = (double*)workspace;
-  if (dtype == ENS_F32) stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, ld, kStatsChunk, part);
-  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, ld, kStatsChunk, part);
+  if (dtype == ENS_F32)
+    stats_partial_kernel<float><<<g, kBlock, 0, s>>>((const float*)x, N, ld, kStatsChunk, part, rows);
+  else stats_partial_kernel<double><<<g, kBlock, 0, s>>>((const double*)x, N, ld, kStatsChunk, part, rows);
   stats_merge_kernel<<<rows, 256, 0, s>>>(part, (int)nparts, stats);
   return cudaPeekAtLastError() == cudaSuccess ? ENS_OK : ENS_E_CUDA;
 }

@@ -11,14 +11,11 @@ namespace ens {
 // a multiple of 16 (block starts are multiples of 128 B). Off by default: on the
 // saveat-dense config the two block barriers per save cost more than the per-thread
 // 8-byte stores they replace (15.9 vs 15.2 ms, profiles/bulk_saves_vs_stg_r01.jsonl);
-// ENS_TUNE_BULK_SAVES=1 enables (tests/test_gpu_saves.py runs it in a subprocess).
+// ens_options.bulk_saves = 1 selects it (tests/test_gpu_saves.py).
 template <class T>
-bool bulk_saves_ok(const Args<T>& a) {
-  static const bool enabled = [] {
-    const char* e = getenv("ENS_TUNE_BULK_SAVES");
-    return e && atoi(e) == 1;
-  }();
-  return enabled && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 && ((size_t)a.ldo * sizeof(T)) % 16 == 0;
+bool bulk_saves_ok(const Args<T>& a, const ens_options* opt) {
+  return opt->bulk_saves == 1 && (reinterpret_cast<uintptr_t>(a.u_out) % 16) == 0 &&
+         ((size_t)a.ldo * sizeof(T)) % 16 == 0;
 }
 
 template <class M, class T>
@@ -32,9 +29,9 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       if (save) {
         // the saving instances hold more registers: pick the block size with the most resident warps
         auto kern = !a.save_grid_only ? tsit5_fixed_kernel<M, f2, 1>
-                    : bulk_saves_ok(a) ? tsit5_fixed_kernel<M, f2, 3> : tsit5_fixed_kernel<M, f2, 2>;
+                    : bulk_saves_ok(a, opt) ? tsit5_fixed_kernel<M, f2, 3> : tsit5_fixed_kernel<M, f2, 2>;
         const dim3 b2(occupancy_block(kern, threads));
-        const size_t smem = (a.save_grid_only && bulk_saves_ok(a)) ? 2 * M::n * b2.x * 2 * sizeof(float) : 0;
+        const size_t smem = (a.save_grid_only && bulk_saves_ok(a, opt)) ? 2 * M::n * b2.x * 2 * sizeof(float) : 0;
         kern<<<dim3((unsigned)cdiv(threads, b2.x)), b2, smem, s>>>(a, cf);
       } else {
         // up to a few waves, the block size with the most resident warps balances the SMs better
@@ -49,9 +46,9 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       const auto cf = make_tsit_coef<double, double>(a.dt0, a.h_last);
       if (save) {
         auto kern = !a.save_grid_only ? tsit5_fixed_kernel<M, double, 1>
-                    : bulk_saves_ok(a) ? tsit5_fixed_kernel<M, double, 3> : tsit5_fixed_kernel<M, double, 2>;
+                    : bulk_saves_ok(a, opt) ? tsit5_fixed_kernel<M, double, 3> : tsit5_fixed_kernel<M, double, 2>;
         const dim3 b(occupancy_block(kern, a.N));
-        const size_t smem = (a.save_grid_only && bulk_saves_ok(a)) ? 2 * M::n * b.x * sizeof(double) : 0;
+        const size_t smem = (a.save_grid_only && bulk_saves_ok(a, opt)) ? 2 * M::n * b.x * sizeof(double) : 0;
         kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, smem, s>>>(a, cf);
       } else {
         const dim3 g = grid_for(a.N), b(solver_block(a.N));

@@ -13,6 +13,7 @@ namespace ens {
 
 struct Lorenz {   // σ(y2−y1), ρy1 − y2 − y1y3, y1y2 − βy3
   static constexpr int n = 3, m = 3, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[3], const T (&p)[m], T, T (&o)[3]) {
     o[0] = p[0] * (y[1] - y[0]);
     o[1] = fmaT(y[0], p[1] - y[2], -y[1]);
@@ -27,6 +28,7 @@ struct Lorenz {   // σ(y2−y1), ρy1 − y2 − y1y3, y1y2 − βy3
 
 struct Robertson {  // P:671-677 with (k1,k2,k3) = p
   static constexpr int n = 3, m = 3, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[3], const T (&p)[m], T, T (&o)[3]) {
     const T r3 = (p[2] * y[1]) * y[2];
     o[0] = fmaT(-p[0], y[0], r3);
@@ -43,6 +45,7 @@ struct Robertson {  // P:671-677 with (k1,k2,k3) = p
 
 template <bool MUL> struct LorenzSDE {  // DESIGN R9: drift = Lorenz, b_j = s (add) or s·u_j (mul)
   static constexpr int n = 3, m = 4, nw = 3;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[3], const T (&p)[m], T, T (&o)[3]) {
     o[0] = p[0] * (y[1] - y[0]);
     o[1] = fmaT(y[0], p[1] - y[2], -y[1]);
@@ -56,6 +59,7 @@ template <bool MUL> struct LorenzSDE {  // DESIGN R9: drift = Lorenz, b_j = s (a
 
 struct GBM {  // dX = rX dt + VX dW (diagonal, 3 independent components)
   static constexpr int n = 3, m = 2, nw = 3;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[3], const T (&p)[m], T, T (&o)[3]) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) o[j] = p[0] * y[j];
@@ -85,6 +89,7 @@ __device__ __forceinline__ void diag_noise(const T (&y)[M::n], const T (&p)[M::m
 // polynomial 2^{n·L(x)} of R2 (x ∈ [1e-30, 1e30], exponent clamped to ±120).
 struct CRN {
   static constexpr int n = 4, m = 6, nw = 8;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static T hill_pow(T x, T e) {
     const T xc = minT(maxT(x, T(1e-30)), T(1e30));
     const T z = minT(maxT(e * log2_spec<T>(xc), T(-120)), T(120));
@@ -132,6 +137,7 @@ struct CRN {
 // downward triggers the affect v ← −e·v; p = (g, e) (DESIGN R18).
 struct Ball {
   static constexpr int n = 2, m = 2, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   static constexpr bool has_event = true;
   template <class T> __device__ __forceinline__ static void f(const T (&y)[2], const T (&p)[2], T, T (&o)[2]) {
     o[0] = y[1];
@@ -157,6 +163,7 @@ __device__ __forceinline__ void apply_noise(const T (&y)[M::n], const T (&p)[M::
 
 struct ExpDecay {  // u' = −λu
   static constexpr int n = 1, m = 1, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[1], const T (&p)[1], T, T (&o)[1]) {
     o[0] = (-p[0]) * y[0];
   }
@@ -167,6 +174,7 @@ struct ExpDecay {  // u' = −λu
 
 struct Harmonic {  // x' = v, v' = −ω²x
   static constexpr int n = 2, m = 1, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   template <class T> __device__ __forceinline__ static void f(const T (&y)[2], const T (&p)[1], T, T (&o)[2]) {
     o[0] = y[1];
     o[1] = -(p[0] * y[0]);

@@ -13,6 +13,7 @@ namespace ens {
 // Oregonator: p = (k1, k2, k3) = (77.27, 8.375e-6, 0.161), y0 = (1, 2, 3), t ∈ [0, 30]
 struct Orego {
   static constexpr int n = 3, m = 3, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   static constexpr bool ad_jac = true;
   template <class Y, class P> __device__ __forceinline__ static void f(const Y (&y)[3], const P (&p)[3], P,
                                                                         Y (&o)[3]) {
@@ -26,6 +27,7 @@ struct Orego {
 // HIRES: p = (1.71, 0.43, 8.32, 0.0007, 8.75, 10.03, 0.035, 1.12, 1.745, 280, 0.69, 1.81)
 struct Hires {
   static constexpr int n = 8, m = 12, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   static constexpr bool ad_jac = true;
   template <class Y, class P> __device__ __forceinline__ static void f(const Y (&y)[8], const P (&p)[12], P,
                                                                         Y (&o)[8]) {
@@ -44,6 +46,7 @@ struct Hires {
 // POLLU, P:779-833 (u9, u16 read as y9, y16): p = k1..k25, 25 reaction rates.
 struct Pollu {
   static constexpr int n = 20, m = 25, nw = 0;
+  static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   static constexpr bool ad_jac = true;
   template <class Y, class P> __device__ __forceinline__ static void f(const Y (&y)[20], const P (&k)[25], P,
                                                                         Y (&o)[20]) {

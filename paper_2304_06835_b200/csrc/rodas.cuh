@@ -91,6 +91,7 @@ __host__ __device__ constexpr double rd_d(int r, int j) {   // r = 0: D2 (s1), r
 template <class Tab, class M, class T>
 __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const T (&u)[M::n],
                                            const T (&F0)[M::n], T (&un)[M::n], T (&K)[Tab::S][M::n]) {
+  ENS_REQUIRE_AUTONOMOUS(M, "Rodas (no γ_i·h·∂f/∂t terms, P:125-136)");
   constexpr int n = M::n, S = Tab::S;
   T W[n][n];
   model_jacobian<M, T>(u, par, t, W);

@@ -104,6 +104,7 @@ template <class M, class T>
 __device__ __forceinline__ bool ros23_step(const T (&par)[M::m], T t, T h, const T (&u)[M::n], const T (&F0)[M::n],
                                            T (&un)[M::n], T (&F2)[M::n], T (&k1)[M::n], T (&k2)[M::n],
                                            T (&E)[M::n]) {
+  ENS_REQUIRE_AUTONOMOUS(M, "Rosenbrock23 (no h·d·∂f/∂t term, P:125-136)");
   constexpr int n = M::n;
   const T d = T(r23_d()), e32 = T(r23_e32());
   T W[n][n];

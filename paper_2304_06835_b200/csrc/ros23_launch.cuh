@@ -2,7 +2,6 @@
 // which holds the POLLU (n = 20) instances: fully unrolled, they are the
 // slowest units to compile, so they build in parallel with the rest).
 #pragma once
-#include <cstdlib>
 #include "launch.cuh"
 #include "ros23.cuh"
 
@@ -18,14 +17,10 @@ ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
     // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
     // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log) — for small systems
     // only: HIRES (n = 8) spills under the cap and runs 17 % slower (profiles/ros23_minb_models_r01.log).
-    // A cap of 4 blocks (64 regs) spills on C3 as well and is slower. ENS_TUNE_ROS23_MINB=1 reverts.
-    static const int minb = [] {
-      const char* e = getenv("ENS_TUNE_ROS23_MINB");
-      return e ? atoi(e) : (sizeof(T) == 8 ? 3 : 1);
-    }();
+    // A cap of 4 blocks (64 regs) spills on C3 as well and is slower.
     // (only when the ensemble fills more than two blocks per SM: a small ensemble — the stiff suite's
     //  8192 — gains no residency from the cap and pays for its spills, OREGO 9 % slower)
-    if (minb == 3 && M::n <= 4 && !opt->refill && a.N > (int64_t)sm_count() * 2 * 256) {
+    if (sizeof(T) == 8 && M::n <= 4 && !opt->refill && a.N > (int64_t)sm_count() * 2 * 256) {
       if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
       else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
     } else {

@@ -78,13 +78,18 @@ __device__ __forceinline__ Moments chan_merge(Moments a, Moments b) {
   return r;
 }
 
-// Partials over a stored [rows][N] array in T: grid (nparts, rows); block b
-// reduces elements [b*chunk, (b+1)*chunk) of its row.
+// gridDim.y is capped at 65535: row-indexed kernels take grid.y = min(rows, kMaxGridY)
+// and stride over their rows (every block of a row does the same work, so the
+// block-wide barriers inside stay uniform).
+constexpr int kMaxGridY = 65535;
+
+// Partials over a stored [rows][N] array in T: grid (nparts, min(rows, 65535));
+// block b reduces elements [b*chunk, (b+1)*chunk) of each of its rows.
 template <class T>
 __global__ void __launch_bounds__(256) stats_partial_kernel(const T* __restrict__ x, int64_t N, int64_t ld,
-                                                            int64_t chunk, double* __restrict__ partial) {
+                                                            int64_t chunk, double* __restrict__ partial, int rows) {
   __shared__ double red[32];
-  const int row = blockIdx.y;
+  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(N, lo + chunk);
   const T* xr = x + (size_t)row * ld;
   double c = 0, s = 0;
@@ -104,6 +109,7 @@ __global__ void __launch_bounds__(256) stats_partial_kernel(const T* __restrict_
   if (threadIdx.x == 0) {
     double* o = partial + ((size_t)row * gridDim.x + blockIdx.x) * 3;
     o[0] = c; o[1] = mean; o[2] = m2;
+  }
   }
 }
 
@@ -136,9 +142,9 @@ static __global__ void __launch_bounds__(256) stats_merge_kernel(const double* _
 // [rows][nblk][3], which stats_merge_kernel then merges. Fixed order throughout.
 constexpr int kFold = 8;
 static __global__ void __launch_bounds__(256) stats_fold_kernel(const double* __restrict__ partial, int64_t nparts,
-                                                         double* __restrict__ out) {
+                                                         double* __restrict__ out, int rows) {
   __shared__ double sc[256], sm[256], s2[256];
-  const int row = blockIdx.y;
+  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
   const double* pr = partial + (size_t)row * nparts * 3;
   const int64_t lo = ((int64_t)blockIdx.x * 256 + threadIdx.x) * kFold;
   Moments acc{0, 0, 0};
@@ -159,6 +165,8 @@ static __global__ void __launch_bounds__(256) stats_fold_kernel(const double* __
   if (threadIdx.x == 0) {
     double* o = out + ((size_t)row * gridDim.x + blockIdx.x) * 3;
     o[0] = sc[0]; o[1] = sm[0]; o[2] = s2[0];
+  }
+  __syncthreads();   // the shared arrays are reused by the next row
   }
 }
 

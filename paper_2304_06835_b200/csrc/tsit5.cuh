@@ -157,8 +157,9 @@ __device__ __forceinline__ void store_lanes(const Args<T>& a, const int64_t (&id
                                             const bool (&live)[LaneOf<V>::W], int j, const V (&v)[n]) {
   if constexpr (LaneOf<V>::W == 2) {
     // a thread's two trajectories are neighbours in memory: one 8-byte store per
-    // component (a warp writes 256 contiguous bytes) when the pair is 8-byte aligned
-    if (live[1] && (a.ldo % 2) == 0 && (reinterpret_cast<uintptr_t>(a.u_out) & 7) == 0) {
+    // component (a warp writes 256 contiguous bytes) when both lanes are live and the
+    // pair is 8-byte aligned (a lane that diverged at t0 keeps its u0 / NaN saves)
+    if (live[0] && live[1] && (a.ldo % 2) == 0 && (reinterpret_cast<uintptr_t>(a.u_out) & 7) == 0) {
 #pragma unroll
       for (int c = 0; c < n; ++c)
         *reinterpret_cast<float2*>(a.u_out + ((size_t)j * n + c) * a.ldo + idx[0]) = v[c].v;
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(256)
   if (SAVE && js < a.k) next = __ldg(a.save_step + js) >> 1;
   // all steps but the last: constant h (no per-step select in the hot loop).
   // Stage times are not needed: the models are autonomous (time argument ignored).
+  ENS_REQUIRE_AUTONOMOUS(M, "fixed-step Tsit5 (stages evaluated at t = 0)");
   for (int64_t s = 0; s + 1 < steps; ++s) {
     tsit5_stages<M, V>(par, splat<V>(T(0)), hdt, ha, u, K, y);
     if (SAVE && next == s + 1) {

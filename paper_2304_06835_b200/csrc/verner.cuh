@@ -105,6 +105,7 @@ struct Vern9Tab {
 template <class Tab, class M, class T, bool WANT_E>
 __device__ __forceinline__ void verner_step(const T (&par)[M::m], T t, T h, const T (&u)[M::n],
                                             T (&K)[Tab::S][M::n], T (&un)[M::n], T (&E)[M::n]) {
+  ENS_REQUIRE_AUTONOMOUS(M, "Vern7 / Vern9 (stages evaluated at the step start time)");
   constexpr int n = M::n, S = Tab::S;
 #pragma unroll
   for (int s = 1; s < S; ++s) {

@@ -164,7 +164,7 @@ def solve(model: str, alg: str, recipe: str, N_total: int, tspan, dt, *, dtype=t
 
     1. shard the N_total trajectories: "contiguous", "block_cyclic" (chunks of `chunk` dealt round-robin,
        one launch per rank through ens_options.chunk_len / chunk_stride), or "auto" (block-cyclic for
-       adaptive runs when N_total divides evenly, contiguous otherwise);
+       adaptive runs when N_total divides evenly and gather != "peer", contiguous otherwise);
     2. generate this shard's inputs on the rank's GPU from (input_seed, global index) — no scatter;
     3. solve the shard (global indices key the Philox noise, so every trajectory is bit-identical for
        any world size);
@@ -179,7 +179,8 @@ def solve(model: str, alg: str, recipe: str, N_total: int, tspan, dt, *, dtype=t
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     adaptive = bool(solve_kw.get("adaptive", False))
     if shard == "auto":
-        shard = "block_cyclic" if adaptive and N_total % (chunk * R) == 0 else "contiguous"
+        # peer gather needs contiguous shards (each rank writes one column slice of dst's array)
+        shard = "block_cyclic" if adaptive and gather != "peer" and N_total % (chunk * R) == 0 else "contiguous"
     if shard == "block_cyclic":
         if gather == "peer":
             raise ValueError("gather='peer' needs contiguous shards")

@@ -26,3 +26,36 @@ def test_reference_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["unit"] == d["unit"]
     assert "workload" in d["config"]
+
+
+def test_parity_sample_inputs_are_the_ensemble_at_those_indices():
+    """bench.py's cpu_baseline sample (global indices i·stride, generated with the
+    block-cyclic map chunk_len = 1) holds exactly the ensemble's inputs there."""
+    import numpy as np
+
+    import bench
+    from synth.inputs import make_inputs
+    for wl in ["c5", "c2"]:
+        recipe, seed, _, _ = bench.WORKLOADS[wl]
+        N_total, sample = 100_003, 777
+        S, stride = bench.sample_indices(N_total, sample)
+        u0s, ps = make_inputs("lorenz", recipe, S, seed=seed, dtype="f32", N_total=N_total, chunk_len=1,
+                              chunk_stride=stride)
+        ug, pg = make_inputs("lorenz", recipe, N_total, seed=seed, dtype="f32")
+        idx = np.arange(S) * stride
+        assert idx[-1] < N_total
+        assert np.array_equal(ps, pg[:, idx]) and np.array_equal(u0s, ug[:, idx])
+
+
+def test_parity_block():
+    import numpy as np
+
+    import bench
+    o = np.random.default_rng(0).standard_normal((3, 50)).astype(np.float32)
+    g = o.copy()
+    g[1, 7] = np.nextafter(g[1, 7], np.float32(np.inf))
+    rc = np.zeros(50, np.int32)
+    b = bench.parity_block(g, rc, o, rc)
+    assert b["n"] == 50 and b["bitexact_frac"] == 49 / 50 and 0 < b["max_rel"] < 1e-6 and b["pass"]
+    b = bench.parity_block(g * 1.001, rc, o, rc)
+    assert not b["pass"]

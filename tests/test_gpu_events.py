@@ -4,7 +4,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -20,9 +20,7 @@ def test_bouncing_ball_parity(dtype, tol, refill):
     o, orc, ona, onr = oracle.solve("ball", "tsit5", u0, p, (0.0, 15.0), 0.1, dtype=dtype, adaptive=True,
                                     abstol=tol, reltol=tol, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999
-    assert traj_relerr(g[..., same], o[..., same]).max() <= (1e-9 if dtype == "f64" else 1e-4)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=(1e-9 if dtype == "f64" else 1e-4))
 
 
 def test_ball_requires_adaptive_tsit5():

@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, sample_indices, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, sample_indices, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -29,10 +29,8 @@ def test_tsit5_fixed_lorenz(dtype, recipe):
     o, orc, ona, _ = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype=dtype)
     assert (rc == 0).all() and (orc == 0).all()
     assert (na == 1000).all() and (ona == 1000).all() and (nr == 0).all()
-    err = traj_relerr(g, o)
-    assert err.max() <= TOL_FIXED[dtype], err.max()
     # canonical operation order on both sides → expected bit-exact
-    assert (g == o).mean() >= 0.99
+    check_fixed(g, o, TOL_FIXED[dtype])
 
 
 @pytest.mark.parametrize("model,u0v,pv", [("expdecay", [1.0], [1.3]), ("harmonic", [1.0, 0.0], [2.25])])
@@ -75,36 +73,41 @@ def test_tsit5_adaptive_lorenz_f64(tol, refill):
     o, orc, ona, onr = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
                                     abstol=tol, reltol=tol)
     assert (rc == 0).all() and (orc == 0).all()
-    same = (na == ona).mean()
-    assert same >= 0.999, same
-    assert traj_relerr(g, o).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
 
 
 def test_tsit5_adaptive_saveat_f64():
     N = 700
     u0, p = make_inputs("lorenz", "random10", N, seed=0xC1, dtype="f64")
     sa = np.linspace(0.0, 1.0, 11)
-    g, rc, na, *_ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10,
-                        saveat=sa)
-    o, orc, ona, _ = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
-                                  abstol=1e-10, reltol=1e-10, saveat=sa)
-    assert (na == ona).mean() >= 0.999
-    assert traj_relerr(g, o).max() <= 1e-8
+    g, rc, na, nr, _ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10,
+                           saveat=sa)
+    o, orc, ona, onr = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
+                                    abstol=1e-10, reltol=1e-10, saveat=sa)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
     np.testing.assert_array_equal(g[0], u0)     # τ = t0 saves u0
 
 
+def fp64_reference(model, alg, u0, p, tspan, dt, tol=1e-12, **kw):
+    """Tight fp64 oracle solution of fp32 inputs (accuracy reference for fp32 adaptive parity)."""
+    ref, *_ = oracle.solve(model, alg, u0.astype(np.float64), p.astype(np.float64), tspan, dt, dtype="f64",
+                           adaptive=True, abstol=tol, reltol=tol, **kw)
+    return ref
+
+
 def test_tsit5_adaptive_f32_sweep():
-    """C2 adaptive (fp32, abstol=reltol=1e-6, ρ sweep)."""
+    """C2 adaptive (fp32, abstol=reltol=1e-6, ρ sweep): identical step counts on
+    ≥ 99.9 % (same controller arithmetic, DESIGN R2), rounding-level agreement
+    where they match, and every trajectory within 1e-4 (≈ 2× the fp32 solutions'
+    own global error against an fp64 1e-12 reference, 5e-5 at this size)."""
     N = 4099
     u0, p = make_inputs("lorenz", "rho_sweep", N, dtype="f32")
     g, rc, na, nr, _ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6)
     o, orc, ona, onr = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
                                     abstol=1e-6, reltol=1e-6)
     assert (rc == orc).all()
-    same = na == ona
-    assert same.mean() >= 0.99, same.mean()
-    # identical step sequences → agreement at fp32 rounding level
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-4
+    ref = fp64_reference("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-4, tol_same=1e-5, ref=ref)
 
 
 def test_refill_is_bitwise_static():
@@ -136,20 +139,20 @@ def test_ros23_robertson_c3_shape(refill):
     o, orc, ona, onr = oracle.solve("robertson", "rosenbrock23", u0, p, (0.0, 1e5), 1e-4, dtype="f64",
                                     adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa)
     assert (rc == 0).all() and (orc == 0).all()
-    assert (na == ona).mean() >= 0.999 and (nr == onr).mean() >= 0.999
-    assert traj_relerr(g, o).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
     assert np.abs(g.sum(1) - 1).max() <= 1e-12     # Σy = 1 (linear invariant)
 
 
 def test_ros23_adaptive_lorenz_f32():
     N = 513
     u0, p = make_inputs("lorenz", "random10", N, seed=9, dtype="f32")
-    g, rc, na, *_ = gpu("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
-    o, orc, ona, _ = oracle.solve("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
-                                  abstol=1e-5, reltol=1e-5)
-    same = na == ona
-    assert same.mean() >= 0.99
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-3
+    g, rc, na, nr, _ = gpu("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5,
+                           reltol=1e-5)
+    o, orc, ona, onr = oracle.solve("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
+                                    abstol=1e-5, reltol=1e-5)
+    ref = fp64_reference("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-3, tol=1e-11)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-2, tol_same=1e-5,
+                   ref=ref)
 
 
 # ------------------------------------------------------------------ EM / SDE --
@@ -165,8 +168,7 @@ def test_em_parity_and_stats(model, dtype):
                                   seed=0xC4, saveat=sa)
     assert (rc == orc).all() and (na == 1000).all()
     # fixed-step tolerance of the north star; the normals are specified to the bit (R8)
-    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
-    assert (g == o).mean() >= 0.99
+    check_fixed(g, o, TOL_FIXED[dtype])
     # fused statistics = definition applied to the GPU's own states (exact-arithmetic bound)
     mean, var, cnt = oracle.stats(g)
     np.testing.assert_allclose(st[..., 1], mean, rtol=1e-13, atol=1e-300)
@@ -259,9 +261,9 @@ def test_retcodes_and_isolation():
 
 @pytest.mark.parametrize("N", [1, 2, 3, 513, 1025])
 def test_paired_fp32_kernels_ragged(N):
-    """fp32 fixed and adaptive kernels carry two trajectories per thread: odd N
-    leaves a dead partner lane; results must equal the oracle and the scalar
-    (refill) path bit for bit."""
+    """The fp32 fixed-step kernel carries two trajectories per thread (FFMA2 pairs):
+    odd N leaves a dead partner lane and a diverged lane sits next to a live
+    partner; results must equal the oracle."""
     u0, p = make_inputs("lorenz", "random10", N, seed=N + 7, dtype="f32")
     u0[0, N // 2] = np.nan                         # a diverged lane next to a live partner
     g, rc, na, nr, _ = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3)
@@ -272,6 +274,31 @@ def test_paired_fp32_kernels_ragged(N):
     if ok.any():
         assert traj_relerr(g[..., ok], o[..., ok]).max() <= TOL_FIXED["f32"]
     np.testing.assert_array_equal(g[..., ~ok], o[..., ~ok])     # diverged lane keeps u0
+
+
+@pytest.mark.parametrize("saves,stats", [(False, False), (True, False), (False, True), (True, True)])
+def test_fp32_pair_lane_diverged_at_t0_even_index(saves, stats):
+    """Finite u0 with a non-finite f(u0) (σ·(y2 − y1) overflows in fp32) at an EVEN
+    index, the first lane of an FFMA2 pair: Diverged with no step, the stored final
+    state is u0 (saves after t0 are NaN), and the fused statistics count u0 for it
+    (R6) — the partner lane's integration must not overwrite it."""
+    N = 130
+    u0, p = make_inputs("lorenz", "random10", N, seed=3, dtype="f32")
+    for i in (0, 64, 128):
+        u0[:, i] = (3e38, -3e38, 0.0)
+    sa = [0.0, 0.25, 1.0] if saves else None
+    g, rc, na, nr, st = gpu("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, saveat=sa, stats=stats)
+    o, orc, ona, onr = oracle.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, dtype="f32", saveat=sa)
+    np.testing.assert_array_equal(rc, orc)
+    assert (rc[[0, 64, 128]] == 3).all() and (na[[0, 64, 128]] == 0).all()
+    np.testing.assert_array_equal(na, ona)
+    bad = np.zeros(N, bool); bad[[0, 64, 128]] = True
+    np.testing.assert_array_equal(g[..., bad], o[..., bad])      # u0 / NaN saves, bit for bit
+    check_fixed(g[..., ~bad], o[..., ~bad], TOL_FIXED["f32"])
+    if stats:
+        mean, var, cnt = oracle.stats(g)
+        np.testing.assert_allclose(st[..., 1], mean, rtol=1e-12)
+        np.testing.assert_allclose(st[..., 2] / (st[..., 0] - 1), var, rtol=1e-10)
 
 
 @pytest.mark.parametrize("N", [1, 31, 32, 33, 255, 257])
@@ -319,7 +346,7 @@ def test_full_size_sampled_parity_bench_config():
     assert (sol.retcode == 0).all().item() and (sol.n_accept == 1000).all().item()
     u0h, ph = make_inputs("lorenz", "rho_sweep", N, dtype="f32")
     o, *_ = oracle.solve("lorenz", "tsit5", u0h[:, idx], ph[:, idx], (0.0, 1.0), 1e-3, dtype="f32")
-    assert traj_relerr(g, o).max() <= 1e-5
+    check_fixed(g, o, 1e-5)
     assert np.isfinite(sol.u.cpu().numpy()).all()
 
 

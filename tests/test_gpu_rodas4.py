@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -28,8 +28,7 @@ def test_rodas4_fixed_parity(model, tf, dt, dtype):
     o, orc, ona, _ = oracle.solve(model, "rodas4", u0, p, (0.0, tf), dt, dtype=dtype, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
     np.testing.assert_array_equal(na, ona)
-    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
-    assert (g == o).mean() >= 0.99          # canonical order on both sides
+    check_fixed(g, o, TOL_FIXED[dtype])
 
 
 @pytest.mark.parametrize("refill", [False, True])
@@ -44,9 +43,7 @@ def test_rodas4_robertson_c3_shape(refill):
     o, orc, ona, onr = oracle.solve("robertson", "rodas4", u0, p, (0.0, 1e5), 1e-4, dtype="f64", adaptive=True,
                                     abstol=1e-8, reltol=1e-8, saveat=sa)
     assert (rc == 0).all() and (orc == 0).all()
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999, same.mean()
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
     assert np.abs(g.sum(1) - 1).max() <= 1e-12     # Σy = 1 (linear invariant)
 
 
@@ -58,9 +55,7 @@ def test_rodas4_adaptive_tight_tolerance_lorenz():
     o, orc, ona, onr = oracle.solve("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
                                     abstol=1e-10, reltol=1e-10)
     np.testing.assert_array_equal(rc, orc)
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999, same.mean()
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
 
 
 @pytest.mark.parametrize("model,tf,N", [("orego", 30.0, 300), ("hires", 321.8122, 500), ("pollu", 60.0, 300)])
@@ -73,10 +68,7 @@ def test_rodas4_stiff_suite_parity(model, tf, N):
                                     abstol=1e-8, reltol=1e-8, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
     assert (rc == 0).mean() > 0.99
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999, same.mean()
-    ok = (rc == 0) & same
-    assert traj_relerr(g[..., ok], o[..., ok]).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
 
 
 def test_rodas4_stiff_references_on_gpu():
@@ -98,12 +90,14 @@ def test_rodas4_stiff_references_on_gpu():
 def test_rodas4_adaptive_lorenz_f32():
     N = 513
     u0, p = make_inputs("lorenz", "random10", N, seed=9, dtype="f32")
-    g, rc, na, *_ = gpu("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
-    o, orc, ona, _ = oracle.solve("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
-                                  abstol=1e-5, reltol=1e-5)
-    same = na == ona
-    assert same.mean() >= 0.99
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-3
+    g, rc, na, nr, _ = gpu("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
+    o, orc, ona, onr = oracle.solve("lorenz", "rodas4", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
+                                    abstol=1e-5, reltol=1e-5)
+    # fp32 at 1e-5: rounding-level agreement where the step counts match; any re-routed
+    # trajectory must be as accurate as the oracle's own (tests/helpers.check_adaptive)
+    ref, *_ = oracle.solve("lorenz", "rodas4", u0.astype(np.float64), p.astype(np.float64), (0.0, 1.0), 1e-3,
+                           dtype="f64", adaptive=True, abstol=1e-11, reltol=1e-11)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-2, tol_same=1e-5, ref=ref)
 
 
 def test_rodas4_ragged_and_single():

@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -21,10 +21,7 @@ def test_stiff_suite_parity(model, tf, N):
                                     abstol=1e-8, reltol=1e-8, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
     assert (rc == 0).mean() > 0.99
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999, same.mean()
-    ok = (rc == 0) & same
-    assert traj_relerr(g[..., ok], o[..., ok]).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
     if model == "hires":
         assert np.abs(g[:, 6] + g[:, 7] - u0[7][None, :]).max() < 1e-15
 

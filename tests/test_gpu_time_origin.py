@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -25,6 +25,4 @@ def test_shifted_tspan(alg, adaptive):
     np.testing.assert_array_equal(rc, orc)
     if not adaptive:
         assert (na == 18).all() and (ona == 18).all()
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999
-    assert traj_relerr(g[..., same], o[..., same]).max() <= (1e-12 if not adaptive else 1e-8)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=(1e-12 if not adaptive else 1e-8))

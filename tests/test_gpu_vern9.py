@@ -5,7 +5,7 @@ import pytest
 
 import oracle
 from synth.inputs import make_inputs
-from tests.helpers import gpu, traj_relerr
+from tests.helpers import check_adaptive, check_fixed, gpu, traj_relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -23,8 +23,7 @@ def test_vern9_fixed_parity(model, tf, dt, dtype):
     o, orc, ona, _ = oracle.solve(model, "vern9", u0, p, (0.0, tf), dt, dtype=dtype, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
     np.testing.assert_array_equal(na, ona)
-    assert traj_relerr(g, o).max() <= TOL_FIXED[dtype]
-    assert (g == o).mean() >= 0.99
+    check_fixed(g, o, TOL_FIXED[dtype])
 
 
 @pytest.mark.parametrize("refill", [False, True])
@@ -37,9 +36,7 @@ def test_vern9_adaptive_tight_tolerance(refill):
     o, orc, ona, onr = oracle.solve("lorenz", "vern9", u0, p, (0.0, 1.0), 1e-3, dtype="f64", adaptive=True,
                                     abstol=1e-10, reltol=1e-10, saveat=sa)
     np.testing.assert_array_equal(rc, orc)
-    same = (na == ona) & (nr == onr)
-    assert same.mean() >= 0.999, same.mean()
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-8
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-8)
 
 
 def test_vern9_ragged_and_f32():
@@ -49,9 +46,11 @@ def test_vern9_ragged_and_f32():
                                     abstol=1e-9, reltol=1e-9)
     assert traj_relerr(g, o).max() <= 1e-8
     u0, p = make_inputs("lorenz", "random10", 333, seed=6, dtype="f32")
-    g, rc, na, *_ = gpu("lorenz", "vern9", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
-    o, orc, ona, _ = oracle.solve("lorenz", "vern9", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
-                                  abstol=1e-5, reltol=1e-5)
-    same = na == ona
-    assert same.mean() >= 0.99
-    assert traj_relerr(g[..., same], o[..., same]).max() <= 1e-3
+    g, rc, na, nr, _ = gpu("lorenz", "vern9", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-5, reltol=1e-5)
+    o, orc, ona, onr = oracle.solve("lorenz", "vern9", u0, p, (0.0, 1.0), 1e-3, dtype="f32", adaptive=True,
+                                    abstol=1e-5, reltol=1e-5)
+    # fp32 at 1e-5: rounding-level agreement where the step counts match; any re-routed
+    # trajectory must be as accurate as the oracle's own (tests/helpers.check_adaptive)
+    ref, *_ = oracle.solve("lorenz", "vern9", u0.astype(np.float64), p.astype(np.float64), (0.0, 1.0), 1e-3,
+                           dtype="f64", adaptive=True, abstol=1e-11, reltol=1e-11)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-2, tol_same=1e-5, ref=ref)

@@ -53,6 +53,32 @@ def _worker(rank, world, port, q):
             ug, pg = make_inputs("lorenz", "random10", N_total, seed=0xC5)
             gi = sh.global_indices().numpy()
             assert np.array_equal(p, pg[:, gi]) and np.array_equal(u0, ug[:, gi])
+        # bench.py's workloads: C5 strong scaling splits N_total contiguously (every global index
+        # exactly once, shard sizes within one), C2 weak scaling gives every rank N per GPU
+        import bench
+
+        class A:
+            workload, n_total, traj_per_gpu = "c5", 10**8 + 3, 7
+        sh, Nt = bench.workload_sizes(A, rank, world)
+        parts = [None] * world
+        dist.all_gather_object(parts, (sh.index_offset, sh.n_local))
+        assert Nt == A.n_total and sum(n for _, n in parts) == Nt
+        off = 0
+        for o, n in parts:
+            assert o == off
+            off += n
+        assert max(n for _, n in parts) - min(n for _, n in parts) <= 1
+        A.workload = "c2"
+        sh, Nt = bench.workload_sizes(A, rank, world)
+        assert Nt == 7 * world and sh.index_offset == 7 * rank and sh.n_local == 7
+        # a C5 shard's on-device inputs are the slice of the global ensemble (host twin, small N_total)
+        A.workload, A.n_total = "c5", world * 1000 + 1
+        sh, Nt = bench.workload_sizes(A, rank, world)
+        u0, p = make_inputs("lorenz", "random10", sh.n_local, seed=0xC5, index_offset=sh.index_offset, N_total=Nt,
+                            dtype="f32")
+        ug, pg = make_inputs("lorenz", "random10", Nt, seed=0xC5, dtype="f32")
+        lo = sh.index_offset
+        assert np.array_equal(p, pg[:, lo:lo + sh.n_local]) and np.array_equal(u0, ug[:, lo:lo + sh.n_local])
         # multi_gpu.solve rejects inconsistent layouts before any device work
         for kw, msg in [(dict(shard="block_cyclic", gather="peer"), "contiguous"),
                         (dict(shard="diagonal"), "unknown shard"),

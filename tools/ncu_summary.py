@@ -2,6 +2,7 @@
 """Summarise ncu outputs into profiles/ (run here, on the CPU box).
 
   python tools/ncu_summary.py full  gpurun_out/prof_X.ncu-rep  TAG  [N_traj FLOP_per_traj]
+  python tools/ncu_summary.py metrics        (prints the --metrics list for the executed-FLOP counters)
   python tools/ncu_summary.py launches gpurun_out/launches_X.csv TAG
 
 full: key metrics of the captured kernel (time, DRAM bytes, pipe / issue
@@ -40,6 +41,30 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warp_latency_issue_stalled.ratio", "local_load", "lts__t_bytes.sum"]
 
 
+# executed FP thread-instructions; pass with --metrics next to --set full
+EXEC_METRICS = ["sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd_pred_on.sum",
+                "sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "sm__sass_thread_inst_executed_op_ffma2_pred_on.sum",
+                "sm__sass_thread_inst_executed_op_fadd2_pred_on.sum", "sm__sass_thread_inst_executed_op_fmul2_pred_on.sum",
+                "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "sm__sass_thread_inst_executed_op_dadd_pred_on.sum",
+                "sm__sass_thread_inst_executed_op_dmul_pred_on.sum"]
+# FLOPs per thread-instruction: an FMA is 2, an add / mul 1; the packed FP32 forms carry two lanes
+EXEC_FLOP = {"ffma": 2, "fadd": 1, "fmul": 1, "ffma2": 4, "fadd2": 2, "fmul2": 2, "dfma": 2, "dadd": 1, "dmul": 1}
+KEYS += EXEC_METRICS
+
+
+def executed_flop(hdr, units, v):
+    """(fp32 FLOP, fp64 FLOP, per-op counts) from the executed-instruction counters, or None."""
+    counts = {}
+    for op in EXEC_FLOP:
+        k = f"sm__sass_thread_inst_executed_op_{op}_pred_on.sum"
+        if k not in hdr:
+            return None
+        counts[op] = float(v[hdr.index(k)].replace(",", ""))
+    f32 = sum(EXEC_FLOP[o] * counts[o] for o in ("ffma", "fadd", "fmul", "ffma2", "fadd2", "fmul2"))
+    f64 = sum(EXEC_FLOP[o] * counts[o] for o in ("dfma", "dadd", "dmul"))
+    return f32, f64, counts
+
+
 def to_bytes(v: str, unit: str) -> float:
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
     return float(v.replace(",", "")) * mult
@@ -64,6 +89,12 @@ def full(rep: str, tag: str, n_traj: float | None, flop: float | None):
         d["time_ms"] = t_ns / 1e6
         if n_traj and flop:
             d["achieved_tflops_under_ncu"] = n_traj * flop / (t_ns * 1e-9) / 1e12
+        ex = executed_flop(hdr, units, v)
+        if ex is not None:
+            d["executed_fp32_flop"], d["executed_fp64_flop"], d["executed_counts"] = ex
+            d["executed_tflops_under_ncu"] = (ex[0] + ex[1]) / (t_ns * 1e-9) / 1e12
+            if n_traj:
+                d["executed_flop_per_traj"] = (ex[0] + ex[1]) / n_traj
         out.append(d)
     PROF.mkdir(exist_ok=True)
     (PROF / f"ncu_full_{tag}.json").write_text(json.dumps(out, indent=1))
@@ -71,6 +102,11 @@ def full(rep: str, tag: str, n_traj: float | None, flop: float | None):
     s = json.loads(summ.read_text()) if summ.exists() else {}
     s[tag] = {"dram_bytes_per_launch": out[0]["dram_bytes_per_launch"], "time_ms": out[0]["time_ms"],
               "kernel": out[0]["kernel"], "source": f"profiles/ncu_full_{tag}.json"}
+    if n_traj:
+        s[tag]["traj_per_launch"] = n_traj
+    if "executed_fp32_flop" in out[0]:
+        s[tag]["executed_flop_per_launch"] = out[0]["executed_fp32_flop"] + out[0]["executed_fp64_flop"]
+        s[tag]["executed_source"] = f"profiles/ncu_full_{tag}.json"
     summ.write_text(json.dumps(s, indent=1))
     print(json.dumps(out[0], indent=1))
 
@@ -97,7 +133,9 @@ def launches(path: str, tag: str):
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "full":
+    if sys.argv[1] == "metrics":
+        print(",".join(EXEC_METRICS))
+    elif sys.argv[1] == "full":
         full(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None,
              float(sys.argv[5]) if len(sys.argv) > 5 else None)
     else:

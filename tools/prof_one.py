@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Run one config a few times (for ncu capture). Usage: prof_one.py NAME [N]
-NAME: c2a (Lorenz tsit5 adaptive fp32 1e-6 rho sweep), c3 (Robertson ros23 fp64
+NAME: c2f32 / c2f64 (Lorenz tsit5 fixed, rho sweep, fused stats), c1t (Lorenz tsit5 fp64 1e-10 rho sweep),
+c2a (Lorenz tsit5 adaptive fp32 1e-6 rho sweep), c3 (Robertson ros23 fp64
 saveat 100), c3r5 (the same on Rodas5), c4 (stochastic Lorenz EM fp32 stats),
 c4d (the same fp64), c1 (Lorenz fp64 adaptive 1e-8), tight9 / tight7 (Lorenz fp64
 1e-10 on Vern9 / Vern7, refill)."""
@@ -26,6 +27,15 @@ elif name in ("c2a_refill", "c2a_shuf", "c2a_shuf_refill"):
     rf = name.endswith("refill")
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6,
                           refill=rf)
+elif name in ("c2f32", "c2f64"):
+    N = N or 10**7
+    dt_ = torch.float32 if name == "c2f32" else torch.float64
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=dt_, N_total=N)
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, stats=True)
+elif name == "c1t":
+    N = N or 10**6
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float64, N_total=N)
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10)
 elif name == "dense":
     N = N or 10**6
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float32, N_total=N)

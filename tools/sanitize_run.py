@@ -4,11 +4,8 @@
 
   compute-sanitizer --tool memcheck python tools/sanitize_run.py
 """
-import os
 import sys
 from pathlib import Path
-
-os.environ.setdefault("ENS_TUNE_BULK_SAVES", "1")   # exercise the cp.async.bulk save path too
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
@@ -29,6 +26,8 @@ for dt in [torch.float32, torch.float64]:
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, saveat=sa, stats=True)
     ub2, pb2 = ens.generate_inputs("lorenz", "random10", 1100, dtype=dt, seed=6)   # full blocks + a tail
     ens.solve("lorenz", "tsit5", ub2, pb2, (0.0, 1.0), 1e-2, saveat=np.arange(0, 101) * 1e-2)   # grid saves
+    ens.solve("lorenz", "tsit5", ub2, pb2, (0.0, 1.0), 1e-2, saveat=np.arange(0, 101) * 1e-2,
+              bulk_saves=True)                                                                  # cp.async.bulk path
     ens.solve("lorenz", "tsit5", ub2, pb2, (0.0, 1.0), 1e-2, saveat=[0.0, 0.333, 1.0])      # interpolated
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True,
