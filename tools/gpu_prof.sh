@@ -10,7 +10,8 @@ mkdir -p $OUT
 python -m paper_2304_06835_b200._build > $OUT/build_$TAG.log 2>&1
 for cs in $CASES; do
   name=${cs%%:*}; kern=${cs#*:}
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kern -s 1 -c 1 \
+  timeout 600 ncu --set full --metrics $(python tools/ncu_summary.py metrics) --clock-control none --import-source on \
+    -k regex:$kern -s 1 -c 1 \
     -o $OUT/prof_${name}_$TAG -f python tools/prof_one.py $name > $OUT/ncu_${name}_$TAG.log 2>&1
 done
 echo done
