@@ -57,9 +57,10 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
       }
     }
   } else {
-    // (a two-trajectories-per-thread f2 variant of the adaptive step measured 4 % slower:
-    //  90 vs 48 registers halves residency, per-lane control flow stays scalar —
-    //  profiles/pair_adaptive_r01.log; the fixed-step kernel is where packing pays)
+    // (a two-trajectories-per-thread f2 variant — packed stage / error / controller arithmetic,
+    //  branch-free per-lane control — issued 194 instead of 281 thread-instructions per attempt,
+    //  but at 94 registers (20 warps per SM) it is latency-bound with the FMA pipe as busy as
+    //  now (66 %): 4.04 ms vs 4.09 ms, 3.98 ms capped at 80 registers; not adopted)
     if (save) launch_adaptive<Tsit5Lane<M, T, true>, T>(a, opt->refill, s);
     else launch_adaptive<Tsit5Lane<M, T, false>, T>(a, opt->refill, s);
   }

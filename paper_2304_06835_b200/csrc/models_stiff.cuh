@@ -13,6 +13,7 @@ namespace ens {
 // Oregonator: p = (k1, k2, k3) = (77.27, 8.375e-6, 0.161), y0 = (1, 2, 3), t ∈ [0, 30]
 struct Orego {
   static constexpr int n = 3, m = 3, nw = 0;
+  static constexpr bool lu_fast_path = false;   // W needs row exchanges often (ros23.cuh lu_factor_fast)
   static constexpr bool autonomous = true;   // f, J (and g) ignore t: ∂f/∂t = 0
   static constexpr bool ad_jac = true;
   template <class Y, class P> __device__ __forceinline__ static void f(const Y (&y)[3], const P (&p)[3], P,

@@ -94,18 +94,20 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
   ENS_REQUIRE_AUTONOMOUS(M, "Rodas (no γ_i·h·∂f/∂t terms, P:125-136)");
   constexpr int n = M::n, S = Tab::S;
   T W[n][n];
-  model_jacobian<M, T>(u, par, t, W);
   const T hg = h * T(Tab::gamma);
   const T ihg = T(1) / hg;
   const T ih = T(1) / h;
-#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
-  for (int i = 0; i < n; ++i)
-#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
-    for (int j = 0; j < n; ++j) W[i][j] = (i == j ? ihg : T(0)) - W[i][j];   // W = I/(hγ) − J
   int piv[n];
   T inv[n];
-  const bool ok = lu_factor<n, T>(W, piv, inv);
-  lu_solve<n, T>(W, piv, inv, F0, K[0]);                                     // k1 = W⁻¹ f(u)
+  bool pm;
+  const bool ok = lu_factor_fast<M, n, T>(W, piv, inv, pm, [&](T (&A)[n][n]) {
+    model_jacobian<M, T>(u, par, t, A);
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+    for (int i = 0; i < n; ++i)
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+      for (int j = 0; j < n; ++j) A[i][j] = (i == j ? ihg : T(0)) - A[i][j];   // W = I/(hγ) − J
+  });
+  lu_solve_w<n, T>(W, piv, inv, pm, F0, K[0]);                               // k1 = W⁻¹ f(u)
   T y[n], F[n], r[n];
 #pragma unroll
   for (int s = 1; s < S; ++s) {
@@ -127,7 +129,7 @@ __device__ __forceinline__ bool rodas_step(const T (&par)[M::m], T t, T h, const
       for (int j = 0; j < s; ++j) acc = fmaT(hc[j], K[j][c], acc);          // f(Y_s) + Σ (c_sj/h) k_j
       r[c] = acc;
     }
-    lu_solve<n, T>(W, piv, inv, r, K[s]);
+    lu_solve_w<n, T>(W, piv, inv, pm, r, K[s]);
   }
 #pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
   for (int c = 0; c < n; ++c) un[c] = y[c] + K[S - 1][c];                    // u_new = Y_S + k_S

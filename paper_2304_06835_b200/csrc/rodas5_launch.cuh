@@ -13,6 +13,12 @@ ens_status run_rodas5(const Args<T>& a, const ens_options* opt, cudaStream_t s) 
   if (!opt->adaptive) {
     if (save) launch_fixed(rodas_grid_fixed_kernel<Rodas5Tab, M, T, true>, a, s);
     else launch_fixed(rodas_grid_fixed_kernel<Rodas5Tab, M, T, false>, a, s);
+  } else if (sizeof(T) == 8 && M::n <= 4 && LuFastPath<M>::value) {
+    // fp64 small systems with the LU fast path: capped at 128 registers (two 256-thread blocks
+    // per SM); uncapped the instance holds 130 and would drop to 12 resident warps (C3: 11.5 vs
+    // 11.0 ms before the cap, 10.6 ms with it)
+    if (save) launch_adaptive<RodasClipLane<Rodas5Tab, M, T, true>, T, 2>(a, opt->refill, s);
+    else launch_adaptive<RodasClipLane<Rodas5Tab, M, T, false>, T, 2>(a, opt->refill, s);
   } else {
     if (save) launch_adaptive<RodasClipLane<Rodas5Tab, M, T, true>, T>(a, opt->refill, s);
     else launch_adaptive<RodasClipLane<Rodas5Tab, M, T, false>, T>(a, opt->refill, s);

@@ -13,19 +13,23 @@ ens_status run_ros23(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   if (!opt->adaptive) {
     if (save) launch_fixed(ros23_fixed_kernel<M, T, true>, a, s);
     else launch_fixed(ros23_fixed_kernel<M, T, false>, a, s);
-  } else {
-    // fp64 Rosenbrock23 is latency-bound at 2 blocks/SM (97 regs); capping registers for a
-    // third resident block is 6 % faster on C3 (profiles/ros23_minb_r01.log) — for small systems
-    // only: HIRES (n = 8) spills under the cap and runs 17 % slower (profiles/ros23_minb_models_r01.log).
-    // A cap of 4 blocks (64 regs) spills on C3 as well and is slower.
-    // (only when the ensemble fills more than two blocks per SM: a small ensemble — the stiff suite's
-    //  8192 — gains no residency from the cap and pays for its spills, OREGO 9 % slower)
-    if (sizeof(T) == 8 && M::n <= 4 && !opt->refill && a.N > (int64_t)sm_count() * 2 * 256) {
-      if (save) launch_adaptive<Ros23Lane<M, T, true>, T, 3>(a, false, s);
-      else launch_adaptive<Ros23Lane<M, T, false>, T, 3>(a, false, s);
+  } else if (opt->refill || M::n > 4) {
+    // refill scheduler, and the larger systems (HIRES / POLLU: the lane form measured 3 % faster
+    // on POLLU than the written-out loop)
+    if (save) launch_adaptive<Ros23Lane<M, T, true>, T>(a, opt->refill, s);
+    else launch_adaptive<Ros23Lane<M, T, false>, T>(a, opt->refill, s);
+  } else if constexpr (M::n <= 4) {
+    // Static mapping of small systems: the written-out loop kernel; fp64 at ≥ 2 blocks of 256
+    // per SM (≤ 128 registers; a cap at 3 blocks / 80 registers spills and was slower with this
+    // loop, 11.91 vs 11.75 ms) when the ensemble fills more than two blocks per SM.
+    if (sizeof(T) == 8 && a.N > (int64_t)sm_count() * 2 * 256) {
+      auto kern = save ? ros23_static_kernel<M, T, true, 2> : ros23_static_kernel<M, T, false, 2>;
+      const dim3 b(occupancy_block(kern, a.N));
+      kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
     } else {
-      if (save) launch_adaptive<Ros23Lane<M, T, true>, T>(a, opt->refill, s);
-      else launch_adaptive<Ros23Lane<M, T, false>, T>(a, opt->refill, s);
+      auto kern = save ? ros23_static_kernel<M, T, true, 1> : ros23_static_kernel<M, T, false, 1>;
+      const dim3 b(occupancy_block(kern, a.N));
+      kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
     }
   }
   return launch_status();

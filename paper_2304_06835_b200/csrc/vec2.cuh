@@ -40,4 +40,29 @@ template <class V> __device__ __forceinline__ V make_lanes(typename LaneOf<V>::T
 template <> __device__ __forceinline__ f2 make_lanes<f2>(float a, float b) { return f2(a, b); }
 template <class V> __device__ __forceinline__ V splat(typename LaneOf<V>::T a) { return make_lanes<V>(a, a); }
 
+// ------------------------------------------------ packed R2 polynomials --
+// log2 of DESIGN R2 on both lanes (Box–Muller radii, R8): the same operations
+// per lane as log2_spec<float>, the polynomial and the quotient refinement as FFMA2.
+// log2_quot on both lanes: two reciprocals, the refinement as FFMA2 (same
+// per-lane rounding as the scalar sequence).
+__device__ __forceinline__ f2 log2_quot2(f2 m) {
+  const f2 a = m - f2(1.0f), b = m + f2(1.0f), nb = -b;
+  f2 r(rcp_approx(b.v.x), rcp_approx(b.v.y));
+  r = fmaT(r, fmaT(nb, r, f2(1.0f)), r);
+  const f2 q = fmaT(a, r, f2(0.0f));
+  return fmaT(r, fmaT(nb, q, a), q);
+}
+__device__ __forceinline__ f2 log2_spec2(float x0, float x1) {
+  int e0, e1;
+  float m0 = frexpT(x0, &e0), m1 = frexpT(x1, &e1);
+  if (m0 < float(0.70710678118654752440)) { m0 = m0 * 2.0f; e0 -= 1; }
+  if (m1 < float(0.70710678118654752440)) { m1 = m1 * 2.0f; e1 -= 1; }
+  const f2 m(m0, m1);
+  const f2 sv = log2_quot2(m);
+  const f2 s2 = sv * sv;
+  f2 acc = f2(pw_lc(PwDeg<float>::L));
+#pragma unroll
+  for (int k = PwDeg<float>::L - 1; k >= 0; --k) acc = fmaT(s2, acc, f2(pw_lc(k)));
+  return fmaT(sv, acc, f2((float)e0, (float)e1));
+}
 }  // namespace ens

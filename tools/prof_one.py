@@ -11,8 +11,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 import paper_2304_06835_b200 as ens
 
-name = sys.argv[1]
-N = int(sys.argv[2]) if len(sys.argv) > 2 else None
+args = [x for x in sys.argv[1:] if not x.startswith("--lib=")]
+for x in sys.argv[1:]:
+    if x.startswith("--lib="):        # an experimental variant (tools/build_variant.py)
+        ens._LIB_PATH = Path(x.split("=", 1)[1]).resolve()
+name = args[0]
+N = int(args[1]) if len(args) > 1 else None
 reps = 3
 if name == "c2a":
     N = N or 10**7
