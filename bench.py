@@ -255,6 +255,14 @@ def parity_block(gpu_states, rc_gpu, oracle_states, rc_oracle):
                                      and (rc_gpu == rc_oracle).all())}
 
 
+def executed_frac(tag: str, n_traj: int, kernel_ms: float, peak_flops: float):
+    """Executed FP FLOP/s of a side measurement as a fraction of the FP peak, from the
+    committed ncu executed-instruction counts of the same workload (profiles/ncu_summary.json),
+    scaled per trajectory; None if no capture is committed."""
+    e = load_executed(tag, n_traj, kernel_ms)
+    return None if e is None else e["tflops"] * 1e12 / peak_flops
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,7 +441,9 @@ def main():
             msf = best_ms(lambda: ens.solve("lorenz", "tsit5", uc, pc, tspan, dt, stream=stream))
             also[f"c2_fixed_{tname}_N1e7"] = {
                 "trajectories_per_s": n_c2 / (msf / 1e3), "kernel_ms": msf,
-                "frac_fp_peak": n_c2 * flops_per_traj(nsteps) / (msf / 1e3) / (pk32 if tname == "f32" else pk64)}
+                "frac_fp_peak": n_c2 * flops_per_traj(nsteps) / (msf / 1e3) / (pk32 if tname == "f32" else pk64),
+                "frac_fp_peak_executed": executed_frac(f"tsit5_fixed_lorenz_{tname}", n_c2, msf,
+                                                       pk32 if tname == "f32" else pk64)}
             if tname == "f32":
                 sol_a = ens.solve("lorenz", "tsit5", uc, pc, tspan, dt, adaptive=True, abstol=1e-6, reltol=1e-6,
                                   stream=stream)
@@ -442,7 +452,8 @@ def main():
                 att = int((sol_a.n_accept.to(torch.int64) + sol_a.n_reject.to(torch.int64)).sum().item())
                 also["c2_adaptive_f32_tol1e-6_N1e7"] = {
                     "trajectories_per_s": n_c2 / (msa / 1e3), "kernel_ms": msa, "attempted_steps_per_traj": att / n_c2,
-                    "frac_fp_peak_265flop_per_attempt": att * 265.0 / (msa / 1e3) / pk32}
+                    "frac_fp_peak_265flop_per_attempt": att * 265.0 / (msa / 1e3) / pk32,
+                    "frac_fp_peak_executed": executed_frac("c2_adaptive_f32", n_c2, msa, pk32)}
                 del sol_a
             del uc, pc
         # NEXT-1: the same ρ sweep in fp64 at the north_star's tight tolerance, Tsit5 vs Vern9
@@ -458,7 +469,10 @@ def main():
             also[f"{alg}_f64_tol1e-10_N{n_t}"] = {"trajectories_per_s": n_t / (mst / 1e3), "kernel_ms": mst,
                                                   "attempted_steps_per_traj": att / n_t,
                                                   f"frac_fp64_peak_{fl:.0f}flop_per_attempt":
-                                                      att * fl / (mst / 1e3) / pk64}
+                                                      att * fl / (mst / 1e3) / pk64,
+                                                  "frac_fp64_peak_executed":
+                                                      executed_frac({"tsit5": "c1t_tsit5_f64_tol1e-10"}.get(alg, ""),
+                                                                    n_t, mst, pk64)}
         del u0t, pt, sol_t
         # NEXT-2: C3 (Robertson fp64, tol 1e-8, 100 save points) on Rosenbrock23 vs Rodas5
         n_s = 10**6
@@ -473,7 +487,8 @@ def main():
             fl = {"rosenbrock23": 170.0, "rodas5": 600.0}[alg]   # ≈ FLOP per attempted Robertson step
             also[f"c3_{alg}_N{n_s}"] = {"trajectories_per_s": n_s / (mss / 1e3), "kernel_ms": mss,
                                         "attempted_steps_per_traj": att / n_s,
-                                        f"frac_fp64_peak_{fl:.0f}flop_per_attempt": att * fl / (mss / 1e3) / pk64}
+                                        f"frac_fp64_peak_{fl:.0f}flop_per_attempt": att * fl / (mss / 1e3) / pk64,
+                                        "frac_fp64_peak_executed": executed_frac(f"c3_{alg}", n_s, mss, pk64)}
             del sol_s
         del ur, pr
 
