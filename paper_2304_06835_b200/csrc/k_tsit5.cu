@@ -61,6 +61,16 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
     //  branch-free per-lane control — issued 194 instead of 281 thread-instructions per attempt,
     //  but at 94 registers (20 warps per SM) it is latency-bound with the FMA pipe as busy as
     //  now (66 %): 4.04 ms vs 4.09 ms, 3.98 ms capped at 80 registers; not adopted)
+    // static mapping without events: the written-out loop kernel (fp64 C1-style ensembles
+    // 4.31 -> 4.10 ms, fp32 C2 adaptive 4.09 -> 4.05 ms; profiles/ab_r02/)
+    if constexpr (!HasEvent<M>::value) {
+      if (!opt->refill) {
+        auto kern = save ? tsit5_static_kernel<M, T, true> : tsit5_static_kernel<M, T, false>;
+        const dim3 b(occupancy_block(kern, a.N));
+        kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
+        return launch_status();
+      }
+    }
     if (save) launch_adaptive<Tsit5Lane<M, T, true>, T>(a, opt->refill, s);
     else launch_adaptive<Tsit5Lane<M, T, false>, T>(a, opt->refill, s);
   }

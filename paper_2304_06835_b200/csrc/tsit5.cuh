@@ -547,6 +547,64 @@ template <class M, class T, bool SAVE> struct Tsit5Lane {
   }
 };
 
+// Static adaptive Tsit5 (one trajectory per thread, models without events), the
+// loop written out with local state: per attempt exactly Tsit5Lane::step's
+// operations, without the lane struct's done flag and early return.
+template <class M, class T, bool SAVE>
+__global__ void __launch_bounds__(256) tsit5_static_kernel(const Args<T> a) {
+  constexpr int n = M::n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  T u[n], par[M::m], K[7][n];
+  load_column<M, T>(a, i, u, par);
+  T t = a.t0, h = a.dt0, lq_old = T(kLFloor);
+  int32_t nacc = 0, nrej = 0, ret = RET_SUCCESS;
+  int js = 0;
+  M::f(u, par, t, K[0]);
+  if (SAVE) {
+    while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
+  }
+  if (!all_finite<n>(K[0])) ret = RET_DIVERGED;
+  else {
+    const int64_t id[1] = {i};
+    const bool lv[1] = {true};
+    while (t < a.tf) {
+      if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; break; }
+      const bool last = (t + h >= a.tf);
+      if (last) h = a.tf - t;
+      T y[n], E[n];
+      const HaReg<T> ha(h);
+      tsit5_stages<M, T>(par, t, h, ha, u, K, y);
+      tsit5_error<n, T>(h, K, E);
+      const T q2 = error_q2<n, T>(E, u, y, a.abstol, a.reltol);
+      if (q2 < T(1)) {
+        const T tn = last ? a.tf : t + h;
+        if (SAVE) tsit5_save<n, T, T>(a, id, lv, js, t, tn, h, u, K, y);
+        t = tn;
+#pragma unroll
+        for (int j = 0; j < n; ++j) { u[j] = y[j]; K[0][j] = K[6][j]; }
+        ++nacc;
+        h = pi_accept<T>(h, q2, lq_old, 7.0 / 50.0, 2.0 / 25.0);
+      } else {
+        h = pi_reject<T>(h, q2, 7.0 / 50.0);
+        ++nrej;
+      }
+      if (t < a.tf && t + h == t) { ret = RET_DTMIN; break; }
+    }
+  }
+  if (SAVE) {
+    T nanv[n];
+#pragma unroll
+    for (int j = 0; j < n; ++j) nanv[j] = nanT<T>();
+    for (; js < a.k; ++js) store_point<n>(a, i, js, nanv);
+  } else {
+    store_point<n>(a, i, 0, u);
+  }
+  if (a.retcode) a.retcode[i] = ret;
+  if (a.nacc) a.nacc[i] = nacc;
+  if (a.nrej) a.nrej[i] = nrej;
+}
+
 // Host-side construction of the fixed-step coefficient table (products in T).
 template <class T, class C>
 inline TsitCoef<C> make_tsit_coef(T h, T hl) {
