@@ -154,8 +154,12 @@ __device__ __forceinline__ bool lu_factor_fast(T (&A)[n][n], int (&piv)[n], T (&
 template <int n, class T>
 __device__ __forceinline__ void lu_solve_w(const T (&LU)[n][n], const int (&piv)[n], const T (&inv)[n], bool permuted,
                                            const T (&b)[n], T (&x)[n]) {
-  if (permuted) lu_solve<n, T, true>(LU, piv, inv, b, x);
-  else lu_solve<n, T, false>(LU, piv, inv, b, x);
+  if constexpr (kBranchSwap<n>) {
+    lu_solve<n, T, true>(LU, piv, inv, b, x);   // n > 4: always lu_factor (no fast path)
+  } else {
+    if (permuted) lu_solve<n, T, true>(LU, piv, inv, b, x);
+    else lu_solve<n, T, false>(LU, piv, inv, b, x);
+  }
 }
 
 // One ode23s step. F0 = f(u,t) (FSAL). Outputs u_new, F2 = f(u_new), k1, k2, E.

@@ -34,10 +34,19 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --metrics $EXEC --clock-control none --import-source on -k regex:tsit5_fixed -s 3 -c 1 \
   -o $OUT/prof_tsit5_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-also \
   > $OUT/ncu_full_$TAG.log 2>&1
-for cs in c2f64:tsit5_fixed c2a:adaptive_static c1t:adaptive_static c3:adaptive_static; do
-  name=${cs%%:*}; kern=${cs#*:}
+python tools/ncu_summary.py full $OUT/prof_tsit5_$TAG.ncu-rep tsit5_fixed_lorenz_f32_$TAG 100000000 192008 \
+  > /dev/null 2>&1 && cp profiles/ncu_full_tsit5_fixed_lorenz_f32_$TAG.json $OUT/
+# executed-FLOP counters of the side kernels: summarised here, the ~10 MB reports are not brought back
+for cs in c2f64:tsit5_fixed:10000000 c2a:static_kernel:10000000 c1t:static_kernel:1000000 \
+          c3:static_kernel:1000000 c3r5:static_kernel:1000000; do
+  IFS=: read name kern n <<< "$cs"
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,$EXEC \
     --clock-control none -k regex:$kern -s 1 -c 1 -o $OUT/prof_exec_${name}_$TAG -f \
     python tools/prof_one.py $name > $OUT/ncu_exec_${name}_$TAG.log 2>&1
+  python tools/ncu_summary.py full $OUT/prof_exec_${name}_$TAG.ncu-rep exec_${name}_$TAG $n > /dev/null 2>&1 \
+    && cp profiles/ncu_full_exec_${name}_$TAG.json $OUT/
+  rm -f $OUT/prof_exec_${name}_$TAG.ncu-rep
 done
+cp profiles/ncu_summary.json $OUT/ncu_summary_box_$TAG.json
+timeout 1200 python tools/bench_configs.py > $OUT/configs_$TAG.jsonl 2> $OUT/configs_$TAG.err
 echo done
