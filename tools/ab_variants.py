@@ -9,7 +9,7 @@ events) and a checksum of the outputs (bit-identity across variants is checked b
 comparing the checksums). Configs: c3 (Robertson Rosenbrock23 fp64 1e-8, saveat
 100, N=10^6), c3r5 / c3r4 (the same on Rodas5 / Rodas4), c2a (Lorenz Tsit5 fp32 1e-6 ρ sweep,
 N=10^7), c1t (Lorenz Tsit5 fp64 1e-10 ρ sweep, N=10^6), t9 (the same on Vern9),
-c2f (Lorenz Tsit5 fixed fp32 10^7), orego/hires/pollu (stiff suite, Rosenbrock23, 8192; suffix 4 / 5:
+c2f (Lorenz Tsit5 fixed fp32 10^7), dense / dense1 (the same with all 1001 grid points saved, N = 4·10^6 / 10^6), orego/hires/pollu (stiff suite, Rosenbrock23, 8192; suffix 4 / 5:
 Rodas4 / Rodas5)."""
 import json
 import subprocess
@@ -40,6 +40,12 @@ elif cfg in ("c1t", "t9"):
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**6, dtype=F64, N_total=10**6)
     alg = "tsit5" if cfg == "c1t" else "vern9"
     f = lambda: ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10)
+elif cfg in ("dense", "dense1"):
+    N = 4 * 10**6 if cfg == "dense" else 10**6
+    u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=F32, N_total=N)
+    sa = [j * 1e-3 for j in range(1001)]
+    sa[-1] = 1.0
+    f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, saveat=sa)
 elif cfg == "c2f":
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**7, dtype=F32, N_total=10**7)
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, stats=True)

@@ -37,6 +37,9 @@ for dt in [torch.float32, torch.float64]:
               saveat=np.linspace(0, 10, 4))
     ens.solve("robertson", "rosenbrock23", ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6,
               refill=True)
+    # Lorenz W = I − h d J needs row exchanges in some warps: the LU fast path's vote + rebuild
+    ens.solve("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
+    ens.solve("lorenz", "rodas5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
     for alg in ["rodas4", "rodas5"]:
         ens.solve("robertson", alg, ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6,
                   saveat=np.linspace(0, 10, 4))
