@@ -8,7 +8,7 @@ variant's library; prints one JSON line with the best-of-R kernel time (CUDA
 events) and a checksum of the outputs (bit-identity across variants is checked by
 comparing the checksums). Configs: c3 (Robertson Rosenbrock23 fp64 1e-8, saveat
 100, N=10^6), c3r5 / c3r4 (the same on Rodas5 / Rodas4), c2a (Lorenz Tsit5 fp32 1e-6 ρ sweep,
-N=10^7), c1t (Lorenz Tsit5 fp64 1e-10 ρ sweep, N=10^6), t9 (the same on Vern9),
+N=10^7), c1t (Lorenz Tsit5 fp64 1e-10 ρ sweep, N=10^6), t9 / t7 (the same on Vern9 / Vern7),
 c2f (Lorenz Tsit5 fixed fp32 10^7), dense / dense1 (the same with all 1001 grid points saved, N = 4·10^6 / 10^6), orego/hires/pollu (stiff suite, Rosenbrock23, 8192; suffix 4 / 5:
 Rodas4 / Rodas5)."""
 import json
@@ -36,9 +36,9 @@ if cfg in ("c3", "c3r5", "c3r4"):
 elif cfg == "c2a":
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**7, dtype=F32, N_total=10**7)
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-6, reltol=1e-6)
-elif cfg in ("c1t", "t9"):
+elif cfg in ("c1t", "t9", "t7"):
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**6, dtype=F64, N_total=10**6)
-    alg = "tsit5" if cfg == "c1t" else "vern9"
+    alg = {"c1t": "tsit5", "t9": "vern9", "t7": "vern7"}[cfg]
     f = lambda: ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10)
 elif cfg in ("dense", "dense1"):
     N = 4 * 10**6 if cfg == "dense" else 10**6
