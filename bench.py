@@ -574,6 +574,10 @@ def main():
                               "sample": f"cpu_baseline sample: global indices i*{stride}, compared element by element"}
         print(json.dumps(line), flush=True)
     if world > 1:
+        # release every rank's CUDA IPC mapping of rank 0's gather array before rank 0 exits
+        del sol, full_states, gathered, peer
+        torch.cuda.synchronize(dev)
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -29,6 +29,10 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
   --master-port 29534 bench.py --gpus 2 --steps 3 --warmup 3 --backend gloo --no-also --no-e2e \
   > $OUT/bench_gloo2_$TAG.json 2> $OUT/bench_gloo2_$TAG.err
+# eight gloo ranks sharing the GPU: the 8-GPU strong-scaling shard arithmetic and fused gather end to end
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
+  --master-port 29535 bench.py --gpus 8 --steps 1 --warmup 3 --backend gloo --no-also --no-e2e \
+  > $OUT/bench_gloo8_$TAG.json 2> $OUT/bench_gloo8_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-also > $OUT/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --metrics $EXEC --clock-control none --import-source on -k regex:tsit5_fixed -s 3 -c 1 \
