@@ -37,9 +37,9 @@ __host__ __device__ constexpr double v7_b(int j) {
   return B[j];
 }
 __host__ __device__ constexpr double v7_bt(int j) {   // b − b̂ (R21)
-  constexpr double BT[10] = {0.0030925885828119940, 0, 0, -0.011727248681971966, 0.051075082200004638,
-                             -0.080965757291055731, 0.32177553732670404, -0.35734362573070983,
-                             0.098735890663364916, -0.024642467069148059};
+  constexpr double BT[10] = {0.0025470118799321617, 0, 0, -0.0096583948727968315, 0.042064709756393717,
+                             -0.066682243746923789, 0.26500974646212530, -0.29430311714032503,
+                             0.081317472324950901, -0.020295184663356433};
   return BT[j];
 }
 
@@ -78,10 +78,10 @@ __host__ __device__ constexpr double v9_b(int j) {
   return B[j];
 }
 __host__ __device__ constexpr double v9_bt(int j) {   // b − b̂ (R21)
-  constexpr double BT[16] = {-0.0053579882904445780, 0, 0, 0, 0, 0, 0, -2.5830204911777926, 0.14252253154675679,
-                             0.013420653512693399, -0.028672962914105127, 2.6249996552108000,
-                             -0.28255096432831926, 0.13643174034775387, 0.030570139830719485,
-                             -0.048342313738061889};
+  constexpr double BT[16] = {-0.0053579882904629451, 0, 0, 0, 0, 0, 0, -2.5830204911866472,
+                             0.14252253154724535, 0.013420653512739405, -0.028672962914203417,
+                             2.6249996552197984, -0.28255096432928784, 0.13643174034822156,
+                             0.030570139830824279, -0.048342313738227605};
   return BT[j];
 }
 

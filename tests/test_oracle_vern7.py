@@ -2,9 +2,11 @@
 
 The tableau is checked against Butcher's rooted-tree order conditions
 (tests/order_conditions.py) (all 85 trees of order ≤ 7 for b, all 37 of order ≤ 6 for the
-embedded b̂ = b − b̃), against measured convergence orders on a closed-form and a
-nonlinear problem, and the saveat rule (step clipping) against plain runs to the
-same end time.
+embedded b̂ = b − b̃), the embedded scale against the structural zeros
+b̂8 = b̂9 = 0 of Verner's 7(6) design (the order conditions leave one free
+scale; one zero fixes it and the other must then vanish too), against measured
+convergence orders on a closed-form and a nonlinear problem, and the saveat
+rule (step clipping) against plain runs to the same end time.
 """
 import math
 
@@ -31,7 +33,22 @@ def test_vern7_order_conditions():
         assert _max_residual(bh, A, k) < 1e-13, k
     assert _max_residual(bh, A, 7) > 1e-5
     assert b[1] == b[2] == bt[1] == bt[2] == 0.0
-    assert abs(bh[0] - 0.044063029903460226) < 1e-17
+
+
+def test_vern7_embedded_scale_structural_zeros():
+    """The embedded pair uses stage 10 (f at the new solution) in place of stages
+    8 and 9: b̂8 = b̂9 = 0. The order-6 conditions fix b̂ − b up to one scale, so the
+    two zeros are one condition plus an independent check (DESIGN R21). A wrong
+    scale (round 1 typed b̂1 = 0.044063…, an error estimate 21 % too large) leaves
+    b̂8 = 0.063, b̂9 = −0.017."""
+    c, A, b, bt = oracle.vern7_tableau()
+    bh = b - bt
+    assert abs(bh[7]) < 1e-15 and abs(bh[8]) < 1e-15, (bh[7], bh[8])
+    assert bt[9] != 0.0 and b[9] == 0.0
+    # the scale is not a free choice any more: rescaling the estimate breaks the zeros
+    for s in [0.9, 1.1]:
+        bhs = b - s * bt
+        assert abs(bhs[7]) > 1e-3 and abs(bhs[8]) > 1e-4
 
 
 def test_vern7_stability_polynomial():

@@ -25,10 +25,10 @@ def test_vern9_order_conditions():
         assert rk_max_residual(bh, A, k) < 1e-13, k
     assert rk_max_residual(bh, A, 9) > 1e-6
     assert (b[1:7] == 0).all() and (bt[1:7] == 0).all() and b[15] == 0
-    # the one-parameter family of order-8 embedded weights, scaled by the published
-    # b̂1, lands on Verner's b̂14 = b̂15 = 0 (an independent check of that scale)
-    assert abs(bh[0] - 0.01996996514886773) < 1e-17
-    assert abs(bh[13]) < 1e-11 and abs(bh[14]) < 1e-11
+    # the one-parameter family of order-8 embedded weights with b̂14 = 0 also has
+    # b̂15 = 0 (an independent check of the scale) and the published b̂1
+    assert abs(bh[13]) < 1e-15 and abs(bh[14]) < 1e-13
+    assert abs(bh[0] - 0.01996996514886773) < 5e-14
 
 
 def test_vern9_stability_polynomial():

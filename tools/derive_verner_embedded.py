@@ -6,9 +6,12 @@ efficient" 7(6) and 9(8) pairs (P:319-320 names GPUVern7 / GPUVern9; the
 paper prints no coefficients). The embedded weights b̂ (order p−1) are fixed
 here from the order conditions: b̂ − b must satisfy every homogeneous
 condition of order ≤ p−1 (37 / 200 rooted trees), which on these stages leaves
-exactly one direction δ; its scale is set by the published b̂1. Prints b̃ to
-17 significant digits (the literals in oracle/oracle.cpp and csrc/verner.cuh)
-and the residuals. Uses mpmath at 50 digits; no oracle / library code.
+exactly one direction δ; its scale is fixed by the structural zeros of
+Verner's embedded weights — b̂8 = b̂9 = 0 for the 7(6) pair, b̂14 = b̂15 = 0 for
+the 9(8) pair (1-based): the scale is solved from the first zero and the second
+must then vanish too, an independent check of the direction δ. Prints b̃ to 17
+significant digits (the literals in oracle/oracle.cpp and csrc/verner.cuh),
+the implied b̂1 and the residuals. Uses mpmath at 50 digits; no oracle / library code.
 Usage: python tools/derive_verner_embedded.py [7|9]
 """
 import mpmath as mp
@@ -71,8 +74,8 @@ B9 = {0: "0.014611976858423152", 7: "-0.3915211862331339", 8: "0.231093250028950
       14: "0.030570139830827976"}
 
 METHODS = {
-    7: dict(C=C7, ROWS=ROWS7, B=B7, BHAT1="0.044063029903460226", zero=(1, 2), norm=7),
-    9: dict(C=C9, ROWS=ROWS9, B=B9, BHAT1="0.01996996514886773", zero=(1, 2, 3, 4, 5, 6), norm=11),
+    7: dict(C=C7, ROWS=ROWS7, B=B7, BHAT_ZERO=(7, 8), zero=(1, 2), norm=7),
+    9: dict(C=C9, ROWS=ROWS9, B=B9, BHAT_ZERO=(13, 14), zero=(1, 2, 3, 4, 5, 6), norm=11),
 }
 A, B, S = None, None, 0
 
@@ -146,8 +149,11 @@ def main(p: int):
         delta[j] = x[k]
     delta[m["norm"]] = D(-1)
     res = max(abs(mp.fsum(M[r, j] * delta[j] for j in range(S))) for r in range(M.rows))
-    s = (D(m["BHAT1"]) - B[0]) / delta[0]
+    z0, z1 = m["BHAT_ZERO"]
+    s = -B[z0] / delta[z0]                       # b̂_z0 = b_z0 + s·δ_z0 = 0
     bhat = [B[j] + s * delta[j] for j in range(S)]
+    print(f"# structural zeros: b_hat[{z0 + 1}] = {mp.nstr(bhat[z0], 3)}, b_hat[{z1 + 1}] = {mp.nstr(bhat[z1], 3)}"
+          f" (independent check); implied b_hat1 = {mp.nstr(bhat[0], 17)}")
     btilde = [B[j] - bhat[j] for j in range(S)]
     print(f"# Vern{p}: homogeneous residual of delta: {mp.nstr(res, 5)}")
     rowsum = max(abs(mp.fsum(A[i]) - m["C"][i]) for i in range(S))
