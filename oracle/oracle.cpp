@@ -26,6 +26,8 @@
 // (closed form e^z and a DOP853 reference step, tests/test_oracle_readings.py).
 // The Verner embedded weights' scale is pinned by the structural zeros of
 // Verner's embedded formulas (b̂8 = b̂9 = 0 / b̂14 = b̂15 = 0, DESIGN R21).
+// Tsit5's embedded scale (the order-4 conditions leave one free direction) is
+// Tsitouras' published constant b̃7 = 1/66 (pinned to that value only).
 // Parity unpinned (oracle-vs-GPU only): the PI-controller
 // constants (R2) — the paper does not print them.
 // Plain mode (orc_set_plain, tests only): the controller as printed with libm

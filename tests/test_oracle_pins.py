@@ -58,6 +58,22 @@ def test_tsit5_tableau_order_conditions():
     assert abs(res_h["5a"]) > 1e-4        # fails an order-5 condition (5.8e-4)
 
 
+def test_tsit5_embedded_scale_is_the_published_constant():
+    """The eight order-≤4 conditions on Tsit5's seven stages have a one-dimensional
+    null space, so they fix b̂ = b − b̃ only up to one scale along it (as for any
+    embedded pair; Verner's scales are fixed by structural zeros, R21). Tsit5's
+    scale is Tsitouras' published choice, b̂7 = −1/66 (b̃7 = 1/66 exactly in fp64):
+    the pin here is that literature constant and that b̃ lies on the null direction
+    (the estimate's scale is pinned by the published value only)."""
+    c, A, bt, r = oracle.tsit5_tableau()
+    Ac = A @ c
+    M = np.array([np.ones(7), c, c**2, Ac, c**3, c * Ac, A @ c**2, A @ Ac])
+    sv = np.linalg.svd(M, compute_uv=False)
+    assert (sv > 1e-10).sum() == 6                     # rank 6: a one-dimensional null space
+    assert np.abs(M @ bt).max() < 1e-15                # b̃ on that null direction
+    assert bt[6] == 1.0 / 66.0
+
+
 def test_tsit5_interpolant_conditions():
     """P:318 'free 4th-order interpolation': b_i(1) = b_i and the continuous
     order-4 conditions sum b_i(θ) Φ_i = θ^ρ/γ hold for all θ."""
