@@ -478,13 +478,13 @@ def main():
         n_s = 10**6
         ur, pr = ens.generate_inputs("robertson", "random10", n_s, dtype=torch.float64, seed=0xC3, device=dev)
         sa = [1e5 * j / 99 for j in range(100)]
-        for alg in ["rosenbrock23", "rodas5"]:
+        for alg in ["rosenbrock23", "rodas5", "rodas5p"]:
             sol_s = ens.solve("robertson", alg, ur, pr, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8, reltol=1e-8,
                               saveat=sa, stream=stream)
             mss = best_ms(lambda: ens.solve("robertson", alg, ur, pr, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                                             reltol=1e-8, saveat=sa, out=sol_s, stream=stream))
             att = int((sol_s.n_accept.to(torch.int64) + sol_s.n_reject.to(torch.int64)).sum().item())
-            fl = {"rosenbrock23": 170.0, "rodas5": 600.0}[alg]   # ≈ FLOP per attempted Robertson step
+            fl = {"rosenbrock23": 170.0, "rodas5": 600.0, "rodas5p": 600.0}[alg]   # ≈ FLOP / attempted step
             also[f"c3_{alg}_N{n_s}"] = {"trajectories_per_s": n_s / (mss / 1e3), "kernel_ms": mss,
                                         "attempted_steps_per_traj": att / n_s,
                                         f"frac_fp64_peak_{fl:.0f}flop_per_attempt": att * fl / (mss / 1e3) / pk64,

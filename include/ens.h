@@ -87,8 +87,10 @@ typedef enum {
                               ODE models with n <= 8 and no events */
   ENS_RODAS5 = 6,          /* Rodas5 (Di Marzo), 5th-order stiffly accurate Rosenbrock, L-stable (R22:
                               the method Rodas5P re-optimises); saves as ENS_VERN7; POLLU fp64 only */
-  ENS_VERN9 = 7            /* Verner 9(8), 16 stages, fixed or adaptive (R21); saves and models as
+  ENS_VERN9 = 7,           /* Verner 9(8), 16 stages, fixed or adaptive (R21); saves and models as
                               ENS_VERN7 */
+  ENS_RODAS5P = 8          /* Rodas5P (Steinebach's re-optimised Rodas5; GPURodas5P, Table 4's
+                              reference; R23): same W-form, stage count, saves and models as ENS_RODAS5 */
 } ens_alg;
 
 typedef enum { ENS_F32 = 0, ENS_F64 = 1 } ens_dtype;

@@ -24,7 +24,8 @@ _LIB = _HERE / "liboracle.so"
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4,
           "expdecay": 5, "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10,
           "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6, "vern9": 7}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6, "vern9": 7,
+         "rodas5p": 8}
 DTYPES = {"f32": 0, "f64": 1}
 NP_DTYPE = {"f32": np.float32, "f64": np.float64}
 
@@ -58,6 +59,7 @@ def lib() -> ctypes.CDLL:
         L.orc_rodas4_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_vern7_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_rodas5_tableau.argtypes = [vp, vp, vp]
+        L.orc_rodas5p_tableau.argtypes = [vp, vp, vp]
         L.orc_vern9_tableau.argtypes = [vp, vp, vp, vp]
         L.orc_controller.argtypes = [i32, vp]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
@@ -156,6 +158,13 @@ def rodas5_tableau():
     """(gamma, A[8,8], C[8,8]) of Rodas5 in W-form (DESIGN R22)."""
     g = np.zeros(1); A = np.zeros((8, 8)); C = np.zeros((8, 8))
     lib().orc_rodas5_tableau(_p(g), _p(A), _p(C))
+    return float(g[0]), A, C
+
+
+def rodas5p_tableau():
+    """(gamma, A[8,8], C[8,8]) of Rodas5P in W-form (DESIGN R23)."""
+    g = np.zeros(1); A = np.zeros((8, 8)); C = np.zeros((8, 8))
+    lib().orc_rodas5p_tableau(_p(g), _p(A), _p(C))
     return float(g[0]), A, C
 
 

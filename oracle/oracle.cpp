@@ -49,7 +49,7 @@ constexpr int NMAX = 32;   // largest state / parameter count (POLLU: n = 20, m 
 enum Model { LORENZ = 0, ROBERTSON = 1, LORENZ_SDE_ADD = 2, LORENZ_SDE_MUL = 3,
              GBM = 4, EXPDECAY = 5, HARMONIC = 6, CRN = 7, OREGO = 8, HIRES = 9, POLLU = 10,
              BALL = 11 };
-enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5, RODAS5 = 6, VERN9 = 7 };
+enum Alg { TSIT5 = 0, ROSENBROCK23 = 1, EM = 2, SIEA = 3, RODAS4 = 4, VERN7 = 5, RODAS5 = 6, VERN9 = 7, RODAS5P = 8 };
 enum Ret { RET_SUCCESS = 0, RET_MAXITERS = 1, RET_DTMIN = 2, RET_DIVERGED = 3, RET_SINGULAR = 4 };
 
 struct Dims { int n, m, nw; bool sde; };
@@ -1128,8 +1128,7 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
 // ---------------------------------------------------------------- Rodas5 ----
 // GPURodas5P's base method (NEXT-2; DESIGN R22): Di Marzo's Rodas5,
 // the 8-stage order-5(4) stiffly accurate W-form Rosenbrock method that
-// Rodas5P re-optimises (Rodas5P's own coefficients are not recoverable
-// offline). Same W-form and conventions as Rodas4: Y7 = Y6 + k6, Y8 = Y7 + k7,
+// Rodas5P (below, R23) re-optimises. Same W-form and conventions as Rodas4: Y7 = Y6 + k6, Y8 = Y7 + k7,
 // u_new = Y8 + k8, E = k8. Pinned by the Rosenbrock B-series order conditions
 // (every rooted tree of order ≤ 5; tests/test_oracle_rodas5.py). No dense
 // output is recoverable either: saves clip the step like Vern7 (R21).
@@ -1156,13 +1155,49 @@ static const double RD5_C[8][7] = {
    -6.685968952921985, -5.810979938412932}};
 static const Ctrl CTRL_RODAS5 = {7.0 / 50.0, 2.0 / 25.0, 0.9, 5.0, 0.1, 1e-4};   // p=5
 
-// One Rodas5 step (autonomous models). F0 = f(u). Outputs u_new, E = k8.
+// Rodas5P (GPURodas5P, Table 4's reference; DESIGN R23): Steinebach's
+// re-optimisation of Rodas5 — same 8-stage stiffly accurate W-form structure
+// (Y7 = Y6 + k6, Y8 = Y7 + k7, E = k8), γ = 0.21193756319429014. Coefficients
+// as published; pinned by the Rosenbrock B-series conditions of every rooted tree
+// of order ≤ 5 (main) / ≤ 4 (embedded) to 2e-14 with order 6 violated
+// (tests/test_oracle_rodas5p.py) — a mistyped digit fails them. Saves clip the
+// step like Rodas5 (R22).
+static const double RD5P_GAMMA = 0.21193756319429014;
+static const double RD5P_A[8][7] = {
+  {0, 0, 0, 0, 0, 0, 0},
+  {3.0, 0, 0, 0, 0, 0, 0},
+  {2.849394379747939, 0.45842242204463923, 0, 0, 0, 0, 0},
+  {-6.954028509809101, 2.489845061869568, -10.358996098473584, 0, 0, 0, 0},
+  {2.8029986275628964, 0.5072464736228206, -0.3988312541770524, -0.04721187230404641, 0, 0, 0},
+  {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 0, 0},
+  {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 1.0, 0},
+  {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 1.0,
+   1.0}};
+static const double RD5P_C[8][7] = {
+  {0, 0, 0, 0, 0, 0, 0},
+  {-14.155112264123755, 0, 0, 0, 0, 0, 0},
+  {-17.97296035885952, -2.859693295451294, 0, 0, 0, 0, 0},
+  {147.12150275711716, -1.41221402718213, 71.68940251302358, 0, 0, 0, 0},
+  {165.43517024871676, -0.4592823456491126, 42.90938336958603, -5.961986721573306, 0, 0, 0},
+  {24.854864614690072, -3.0009227002832186, 47.4931110020768, 5.5814197821558125, -0.6610691825249471, 0, 0},
+  {30.91273214028599, -3.1208243349937974, 77.79954646070892, 34.28646028294783, -19.097331116725623,
+   -28.087943162872662, 0},
+  {37.80277123390563, -3.2571969029072276, 112.26918849496327, 66.9347231244047, -40.06618937091002,
+   -54.66780262877968, -9.48861652309627}};
+
+// The 8-stage clipping Rosenbrock tableaus (Rodas5, Rodas5P).
+struct Rd8Tab { double gamma; const double (*A)[7]; const double (*C)[7]; const Ctrl* ctrl; };
+static const Rd8Tab RODAS5_TAB = {RD5_GAMMA, RD5_A, RD5_C, &CTRL_RODAS5};
+static const Rd8Tab RODAS5P_TAB = {RD5P_GAMMA, RD5P_A, RD5P_C, &CTRL_RODAS5};   // p = 5 as well
+
+// One Rodas5 / Rodas5P step (autonomous models). F0 = f(u). Outputs u_new, E = k8.
 template <class T>
-static bool rodas5_step(int model, int n, const T* p, T t, T h, const T* u, const T* F0, T* unew, T* E) {
+static bool rodas5_step(const Rd8Tab& tb, int model, int n, const T* p, T t, T h, const T* u, const T* F0, T* unew,
+                        T* E) {
   T J[NMAX * NMAX], W[NMAX * NMAX], inv[NMAX]; int piv[NMAX];
   T K[8][NMAX];
   jac<T>(model, u, p, t, J);
-  const T hg = h * (T)RD5_GAMMA;
+  const T hg = h * (T)tb.gamma;
   const T ihg = T(1) / hg;                                             // 1/(hγ)
   const T ih = T(1) / h;
   for (int i = 0; i < n; ++i)
@@ -1173,13 +1208,13 @@ static bool rodas5_step(int model, int n, const T* p, T t, T h, const T* u, cons
   for (int s = 1; s < 8; ++s) {
     for (int c = 0; c < n; ++c) {                                      // Y_s = u + Σ_{j<s} a_sj k_j
       T acc = u[c];
-      for (int j = 0; j < s; ++j) acc = std::fma((T)RD5_A[s][j], K[j][c], acc);
+      for (int j = 0; j < s; ++j) acc = std::fma((T)tb.A[s][j], K[j][c], acc);
       y[c] = acc;
     }
     rhs<T>(model, y, p, t, F);
     for (int c = 0; c < n; ++c) {                                      // f(Y_s) + Σ_{j<s} (c_sj/h) k_j
       T acc = F[c];
-      for (int j = 0; j < s; ++j) acc = std::fma((T)RD5_C[s][j] * ih, K[j][c], acc);
+      for (int j = 0; j < s; ++j) acc = std::fma((T)tb.C[s][j] * ih, K[j][c], acc);
       r[c] = acc;
     }
     lu_solve<T>(n, W, piv, inv, r, K[s]);
@@ -1189,9 +1224,9 @@ static bool rodas5_step(int model, int n, const T* p, T t, T h, const T* u, cons
 }
 
 template <class T>
-static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
+static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const int n = tr.n, model = o.model;
-  const Ctrl& C = CTRL_RODAS5;
+  const Ctrl& C = *tb.ctrl;
   T u[NMAX], F0[NMAX], unew[NMAX], E[NMAX];
   for (int j = 0; j < n; ++j) u[j] = tr.u0[j];
   const T* p = tr.p;
@@ -1214,7 +1249,7 @@ static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
       const bool last = (i == nsteps - 1);
       const T h = last ? hl : hdt;
       t = (T)(o.t0 + (double)i * o.dt);
-      if (!rodas5_step<T>(model, n, p, t, h, u, F0, unew, E)) { tr.retcode = RET_SINGULAR; break; }
+      if (!rodas5_step<T>(tb, model, n, p, t, h, u, F0, unew, E)) { tr.retcode = RET_SINGULAR; break; }
       for (int j = 0; j < n; ++j) u[j] = unew[j];
       if (!last) rhs<T>(model, u, p, (T)(o.t0 + (double)(i + 1) * o.dt), F0);
       tr.n_accept++;
@@ -1232,7 +1267,7 @@ static void solve_rodas5(const Opts& o, Traj<T>& tr, const int64_t* save_step) {
       const bool clip = (t + h >= target);
       if (clip) h = target - t;
       ++attempts;
-      if (!rodas5_step<T>(model, n, p, t, h, u, F0, unew, E)) {
+      if (!rodas5_step<T>(tb, model, n, p, t, h, u, F0, unew, E)) {
         h = h * T(0.5);                                   // singular W: reject, halve (DESIGN R10)
         tr.n_reject++;
         if (t + h == t) { tr.retcode = RET_SINGULAR; break; }
@@ -1554,7 +1589,8 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM || o.alg == SIEA || ((o.alg == VERN7 || o.alg == VERN9 || o.alg == RODAS5) && !o.adaptive)) {
+  if (o.alg == EM || o.alg == SIEA ||
+      ((o.alg == VERN7 || o.alg == VERN9 || o.alg == RODAS5 || o.alg == RODAS5P) && !o.adaptive)) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);
@@ -1575,7 +1611,8 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
     else if (o.alg == RODAS4) solve_rodas4<T>(o, tr);
     else if (o.alg == VERN7) solve_verner<T>(VERN7_TAB, o, tr, save_step.data());
     else if (o.alg == VERN9) solve_verner<T>(VERN9_TAB, o, tr, save_step.data());
-    else if (o.alg == RODAS5) solve_rodas5<T>(o, tr, save_step.data());
+    else if (o.alg == RODAS5) solve_rodas5<T>(RODAS5_TAB, o, tr, save_step.data());
+    else if (o.alg == RODAS5P) solve_rodas5<T>(RODAS5P_TAB, o, tr, save_step.data());
     else if (o.alg == SIEA) solve_siea<T>(o, tr, save_step.data());
     else solve_em<T>(o, tr, save_step.data());
     for (int s = 0; s < kk; ++s)
@@ -1627,7 +1664,7 @@ void orc_tsit5_tableau(double* c, double* A, double* btilde, double* r) {
 void orc_ros23_consts(double* d, double* e32) { *d = orc::R23_D; *e32 = orc::R23_E32; }
 static const orc::Ctrl& ctrl_of(int alg) {
   return alg == orc::ROSENBROCK23 ? orc::CTRL_ROS23 : alg == orc::RODAS4 ? orc::CTRL_RODAS4
-       : alg == orc::VERN7 ? orc::CTRL_VERN7 : alg == orc::RODAS5 ? orc::CTRL_RODAS5
+       : alg == orc::VERN7 ? orc::CTRL_VERN7 : (alg == orc::RODAS5 || alg == orc::RODAS5P) ? orc::CTRL_RODAS5
        : alg == orc::VERN9 ? orc::CTRL_VERN9 : orc::CTRL_TSIT5;
 }
 // Rodas4 tableau export for the order-condition pins: gamma, A[36], C[36] (6×6 row-major, strictly lower), D[10].
@@ -1646,6 +1683,15 @@ void orc_vern7_tableau(double* c, double* A, double* b, double* bt) {
     c[i] = orc::V7_C[i]; b[i] = orc::V7_B[i]; bt[i] = orc::V7_BT[i];
     for (int j = 0; j < 10; ++j) A[i * 10 + j] = j < 9 ? orc::V7_A[i][j] : 0.0;
   }
+}
+// Rodas5P tableau export: gamma, A[64], C[64] (8×8 row-major, strictly lower).
+void orc_rodas5p_tableau(double* gamma, double* A, double* C) {
+  *gamma = orc::RD5P_GAMMA;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      A[i * 8 + j] = j < 7 ? orc::RD5P_A[i][j] : 0.0;
+      C[i * 8 + j] = j < 7 ? orc::RD5P_C[i][j] : 0.0;
+    }
 }
 // Rodas5 tableau export: gamma, A[64], C[64] (8×8 row-major, strictly lower).
 void orc_rodas5_tableau(double* gamma, double* A, double* C) {

@@ -22,7 +22,8 @@ _LIB_PATH = _PKG / "libens.so"
 
 MODELS = {"lorenz": 0, "robertson": 1, "lorenz_sde_add": 2, "lorenz_sde_mul": 3, "gbm": 4, "expdecay": 5,
           "harmonic": 6, "crn": 7, "orego": 8, "hires": 9, "pollu": 10, "ball": 11}
-ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6, "vern9": 7}
+ALGS = {"tsit5": 0, "rosenbrock23": 1, "em": 2, "siea": 3, "rodas4": 4, "vern7": 5, "rodas5": 6, "vern9": 7,
+         "rodas5p": 8}
 DTYPES = {torch.float32: 0, torch.float64: 1}
 RECIPES = {"random10": 0, "rho_sweep": 1, "const": 2, "grid": 3}
 RETCODES = {0: "Success", 1: "MaxIters", 2: "DtLessThanMin", 3: "Diverged", 4: "Singular"}

@@ -69,7 +69,8 @@ bool model_dims(int model, int* n, int* m, int* nw) {
 inline bool is_sde_alg(int alg) { return alg == ENS_EM || alg == ENS_SIEA; }
 // save points given as step-grid indices (DESIGN R11; fixed-step Vern7 / Rodas5, R21-R22)
 inline bool grid_saves(int alg, const ens_options* opt) {
-  return is_sde_alg(alg) || ((alg == ENS_VERN7 || alg == ENS_VERN9 || alg == ENS_RODAS5) && !opt->adaptive);
+  return is_sde_alg(alg) ||
+         ((alg == ENS_VERN7 || alg == ENS_VERN9 || alg == ENS_RODAS5 || alg == ENS_RODAS5P) && !opt->adaptive);
 }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -125,6 +126,7 @@ ens_status dispatch(int model, int alg, const Args<T>& a, const ens_options* opt
     case ENS_VERN7: return launch_vern7<T>(model, a, opt, s);
     case ENS_RODAS5: return launch_rodas5<T>(model, a, opt, s);
     case ENS_VERN9: return launch_vern9<T>(model, a, opt, s);
+    case ENS_RODAS5P: return launch_rodas5p<T>(model, a, opt, s);
     case ENS_EM: case ENS_SIEA: return launch_sde<T>(model, alg, a, opt, s);
   }
   return ENS_E_INVALID_ARG;
@@ -135,7 +137,7 @@ ens_status validate(int model, int alg, int dtype, int64_t N, double t0, double 
                     const ens_options* opt, int* n_out) {
   int n, m, nw;
   if (!opt || N < 1 || !model_dims(model, &n, &m, &nw)) return ENS_E_INVALID_ARG;
-  if (alg < ENS_TSIT5 || alg > ENS_VERN9 || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
+  if (alg < ENS_TSIT5 || alg > ENS_RODAS5P || (dtype != ENS_F32 && dtype != ENS_F64)) return ENS_E_INVALID_ARG;
   if (opt->n_saveat < 0 || (opt->n_saveat > 0 && !opt->saveat)) return ENS_E_INVALID_ARG;
   if (opt->chunk_len < 0 || opt->index_offset < 0) return ENS_E_INVALID_ARG;
   if (opt->out_ld != 0 && opt->out_ld < N) return ENS_E_INVALID_ARG;

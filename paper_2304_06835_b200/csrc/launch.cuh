@@ -1,6 +1,7 @@
 // launch.cuh — launch configuration shared by the per-algorithm translation
-// units (k_tsit5.cu, k_vern7.cu, k_vern9.cu, k_ros23.cu, k_rodas4.cu, k_rodas5.cu, k_sde.cu, and the
-// POLLU units k_ros23_pollu.cu, k_rodas4_pollu.cu, k_rodas5_pollu.cu) and the ABI (api.cu).
+// units (k_tsit5.cu, k_vern7.cu, k_vern9.cu, k_ros23.cu, k_rodas4.cu, k_rodas5.cu, k_rodas5p.cu, k_sde.cu,
+// and the POLLU units k_ros23_pollu.cu, k_rodas4_pollu.cu, k_rodas5_pollu.cu, k_rodas5p_pollu.cu) and the
+// ABI (api.cu).
 // Each algorithm's kernel instances live in their own .cu so the library
 // builds in parallel; api.cu only sees the launch_* entry points below.
 #pragma once
@@ -103,6 +104,7 @@ template <class T> ens_status launch_ros23(int model, const Args<T>& a, const en
 template <class T> ens_status launch_rodas4(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s);
 template <class T> ens_status launch_vern7(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s);
 template <class T> ens_status launch_rodas5(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s);
+template <class T> ens_status launch_rodas5p(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s);
 template <class T> ens_status launch_vern9(int model, const Args<T>& a, const ens_options* opt, cudaStream_t s);
 template <class T> ens_status launch_sde(int model, int alg, const Args<T>& a, const ens_options* opt, cudaStream_t s);
 

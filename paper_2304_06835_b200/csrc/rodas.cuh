@@ -1,6 +1,6 @@
 // rodas.cuh — per-thread W-form Rosenbrock integrators for sm_100a:
-// Rodas4 (GPURodas4; DESIGN R20) and Rodas5 (the method GPURodas5P
-// re-optimises; DESIGN R22). NEXT-2.
+// Rodas4 (GPURodas4; DESIGN R20), Rodas5 (DESIGN R22) and its
+// re-optimisation Rodas5P (GPURodas5P; DESIGN R23). NEXT-2.
 //
 // One exact Jacobian per step (analytic or in-kernel forward AD), one
 // in-register LU of W = I/(hγ) − J, S triangular solves and S RHS evaluations
@@ -64,6 +64,38 @@ __host__ __device__ constexpr double rd5_c(int s, int j) {
   return C[s][j];
 }
 
+// Rodas5P (Steinebach's re-optimisation of Rodas5; GPURodas5P; DESIGN R23):
+// same stage structure (Y7 = Y6 + k6, Y8 = Y7 + k7), γ = 0.21193756319429014.
+__host__ __device__ constexpr double rd5p_a(int s, int j) {
+  constexpr double A[8][7] = {
+      {0, 0, 0, 0, 0, 0, 0},
+      {3.0, 0, 0, 0, 0, 0, 0},
+      {2.849394379747939, 0.45842242204463923, 0, 0, 0, 0, 0},
+      {-6.954028509809101, 2.489845061869568, -10.358996098473584, 0, 0, 0, 0},
+      {2.8029986275628964, 0.5072464736228206, -0.3988312541770524, -0.04721187230404641, 0, 0, 0},
+      {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 0,
+       0},
+      {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 1.0,
+       0},
+      {-7.502846399306121, 2.561846144803919, -11.627539656261098, -0.18268767659942256, 0.030198172008377946, 1.0,
+       1.0}};
+  return A[s][j];
+}
+__host__ __device__ constexpr double rd5p_c(int s, int j) {
+  constexpr double C[8][7] = {
+      {0, 0, 0, 0, 0, 0, 0},
+      {-14.155112264123755, 0, 0, 0, 0, 0, 0},
+      {-17.97296035885952, -2.859693295451294, 0, 0, 0, 0, 0},
+      {147.12150275711716, -1.41221402718213, 71.68940251302358, 0, 0, 0, 0},
+      {165.43517024871676, -0.4592823456491126, 42.90938336958603, -5.961986721573306, 0, 0, 0},
+      {24.854864614690072, -3.0009227002832186, 47.4931110020768, 5.5814197821558125, -0.6610691825249471, 0, 0},
+      {30.91273214028599, -3.1208243349937974, 77.79954646070892, 34.28646028294783, -19.097331116725623,
+       -28.087943162872662, 0},
+      {37.80277123390563, -3.2571969029072276, 112.26918849496327, 66.9347231244047, -40.06618937091002,
+       -54.66780262877968, -9.48861652309627}};
+  return C[s][j];
+}
+
 // Tableau traits: S stages, γ, W-form a / c, PI exponents (R2 rule, p = order).
 struct Rodas4Tab {
   static constexpr int S = 6;
@@ -76,6 +108,12 @@ struct Rodas5Tab {
   static constexpr double gamma = 0.19, beta1 = 7.0 / 50.0, beta2 = 2.0 / 25.0;
   __host__ __device__ static constexpr double a(int s, int j) { return rd5_a(s, j); }
   __host__ __device__ static constexpr double c(int s, int j) { return rd5_c(s, j); }
+};
+struct Rodas5PTab {
+  static constexpr int S = 8;
+  static constexpr double gamma = 0.21193756319429014, beta1 = 7.0 / 50.0, beta2 = 2.0 / 25.0;
+  __host__ __device__ static constexpr double a(int s, int j) { return rd5p_a(s, j); }
+  __host__ __device__ static constexpr double c(int s, int j) { return rd5p_c(s, j); }
 };
 
 __host__ __device__ constexpr double rd_d(int r, int j) {   // r = 0: D2 (s1), r = 1: D3 (s2)

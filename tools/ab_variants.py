@@ -28,10 +28,10 @@ var, cfg = sys.argv[1], sys.argv[2]
 if var != "base":
     ens._LIB_PATH = Path("paper_2304_06835_b200/_variants") / var / "libens.so"
 F64, F32 = torch.float64, torch.float32
-if cfg in ("c3", "c3r5", "c3r4"):
+if cfg in ("c3", "c3r5", "c3r4", "c3r5p"):
     u0, p = ens.generate_inputs("robertson", "random10", 10**6, dtype=F64, seed=0xC3)
     sa = [1e5 * j / 99 for j in range(100)]
-    alg = {"c3": "rosenbrock23", "c3r5": "rodas5", "c3r4": "rodas4"}[cfg]
+    alg = {"c3": "rosenbrock23", "c3r5": "rodas5", "c3r4": "rodas4", "c3r5p": "rodas5p"}[cfg]
     f = lambda: ens.solve("robertson", alg, u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa)
 elif cfg == "c2a":
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**7, dtype=F32, N_total=10**7)

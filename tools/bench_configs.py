@@ -138,6 +138,8 @@ def main():
     for refill in [False, True]:
         run("C3-rodas5", "robertson", "rodas5", "random10", 10**6, "f64", (0.0, 1e5), 1e-4, None, reps=3,
             input_seed=0xC3, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa, refill=refill)
+        run("C3-rodas5p", "robertson", "rodas5p", "random10", 10**6, "f64", (0.0, 1e5), 1e-4, None, reps=3,
+            input_seed=0xC3, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa, refill=refill)
     # C4: stochastic Lorenz EM dt=1e-3, 10^6 paths, 11 save points, ensemble mean/var
     sa4 = [j / 10 for j in range(11)]
     for model in ["lorenz_sde_add", "lorenz_sde_mul"]:
@@ -153,7 +155,7 @@ def main():
     for model, tf in [("orego", 30.0), ("hires", 321.8122), ("pollu", 60.0)]:
         run("stiff-" + model, model, "rosenbrock23", "random10", 8192, "f64", (0.0, tf), 1e-6, "ros23", reps=3,
             input_seed=0x57, adaptive=True, abstol=1e-8, reltol=1e-8)
-        for alg in ["rodas4", "rodas5"]:
+        for alg in ["rodas4", "rodas5", "rodas5p"]:
             run(f"stiff-{alg}-" + model, model, alg, "random10", 8192, "f64", (0.0, tf), 1e-6, None, reps=3,
                 input_seed=0x57, adaptive=True, abstol=1e-8, reltol=1e-8)
     # C5: Lorenz fp32 10^8 on one GPU (the 8-GPU run shards this), random p ±10 %
