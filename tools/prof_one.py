@@ -56,11 +56,12 @@ elif name == "c3":
     sa = [1e5 * j / 99 for j in range(100)]
     f = lambda: ens.solve("robertson", "rosenbrock23", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                           reltol=1e-8, saveat=sa)
-elif name == "c3r5":
+elif name in ("c3r5", "c3r5p"):
     N = N or 10**6
     u0, p = ens.generate_inputs("robertson", "random10", N, dtype=torch.float64, seed=0xC3)
     sa = [1e5 * j / 99 for j in range(100)]
-    f = lambda: ens.solve("robertson", "rodas5", u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
+    alg = "rodas5" if name == "c3r5" else "rodas5p"
+    f = lambda: ens.solve("robertson", alg, u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                           reltol=1e-8, saveat=sa)
 elif name in ("tight9", "tight7"):
     N = N or 10**6
