@@ -577,6 +577,7 @@ def main():
         # release every rank's CUDA IPC mapping of rank 0's gather array before rank 0 exits
         del sol, full_states, gathered, peer
         torch.cuda.synchronize(dev)
+        torch.cuda.ipc_collect()
         dist.barrier()
         dist.destroy_process_group()
 
