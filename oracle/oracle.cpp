@@ -74,10 +74,11 @@ static bool dims(int model, Dims* d) {
 template <class T> static T log2_spec(T x);
 template <class T> static T exp2_spec(T z);
 
-// "Plain" mode (test-only cross-check of readings R2 and R8, set by
-// orc_set_plain): the PI controller is evaluated literally as printed at P:120
-// with libm pow on q = sqrt(q²), and Box–Muller with libm
-// log / sqrt / sin / cos. Default 0 = the canonical exponent-domain / polynomial
+// "Plain" mode (test-only cross-check of readings R1, R2 and R8, set by
+// orc_set_plain): Tsit5's stage sums as y = u + h·Σ a_il k_l
+// instead of R1's u + Σ (h·a_il) k_l; the PI controller evaluated literally as
+// printed at P:120 with libm pow on q = sqrt(q²); Box–Muller with
+// libm log / sqrt / sin / cos. Default 0 = the canonical exponent-domain / polynomial
 // forms that the kernels follow. The test suite runs both modes on
 // the same ensembles to measure what the readings change (DESIGN R2, R8).
 static int g_plain = 0;
@@ -569,6 +570,12 @@ static void tsit5_step(int model, int n, const T* p, T t, T h, const T* u, T K[7
   T y[NMAX];
   for (int i = 1; i < 7; ++i) {
     for (int j = 0; j < n; ++j) {
+      if (g_plain) {   // plain mode: the stage sum as printed, y = u + h·Σ_l a_il k_l
+        T acc = (T)TS_A[i][0] * K[0][j];
+        for (int l = 1; l < i; ++l) acc = std::fma((T)TS_A[i][l], K[l][j], acc);
+        y[j] = std::fma(h, acc, u[j]);
+        continue;
+      }
       T acc = u[j];
       for (int l = 0; l < i; ++l) acc = std::fma(h * (T)TS_A[i][l], K[l][j], acc);
       y[j] = acc;
