@@ -587,6 +587,6 @@ const char* ens_status_string(ens_status s) {
   return "unknown status";
 }
 
-const char* ens_version(void) { return "ens-b200 0.1 (sm_100a)"; }
+const char* ens_version(void) { return "ens-b200 0.2 (sm_100a)"; }
 
 }  // extern "C"

@@ -107,3 +107,33 @@ def test_generate_inputs_validation():
     assert L.ens_generate_inputs(ens.MODELS["robertson"], 0, 1, 0, 10, 10, None, fake, fake, None) == 8
     assert L.ens_generate_inputs(ens.MODELS["lorenz"], 0, 7, 0, 10, 10, None, fake, fake, None) == 1
     assert L.ens_generate_inputs(ens.MODELS["lorenz"], 0, 0, 0, 0, 10, None, fake, fake, None) == 1
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of ens_options / ens_output have the C header's
+    size and field offsets (compiled from include/ens.h with the host compiler)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    import paper_2304_06835_b200 as ens
+    cxx = shutil.which("g++") or shutil.which("c++")
+    if not cxx:
+        import pytest
+        pytest.skip("no host C++ compiler")
+    inc = ROOT / "include"
+    fields = [f for f, _ in ens._Options._fields_]
+    ofields = [f for f, _ in ens._Output._fields_]
+    src = tmp_path / "layout.cpp"
+    src.write_text('#include <cstdio>\n#include <cstddef>\n#include "ens.h"\nint main(){\n'
+                   + 'printf("%zu\\n", sizeof(ens_options));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(ens_options, {f}));\n' for f in fields)
+                   + 'printf("%zu\\n", sizeof(ens_output));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(ens_output, {f}));\n' for f in ofields)
+                   + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call([cxx, "-I", str(inc), "-o", str(exe), str(src)])
+    vals = [int(x) for x in subprocess.check_output([str(exe)], text=True).split()]
+    want = ([ctypes.sizeof(ens._Options)] + [getattr(ens._Options, f).offset for f in fields]
+            + [ctypes.sizeof(ens._Output)] + [getattr(ens._Output, f).offset for f in ofields])
+    assert vals == want, (vals, want)
