@@ -5,6 +5,11 @@
 #include "launch.cuh"
 #include "tsit5.cuh"
 
+// A/B builds only (tools/build_variant.py -DENS_NO_PAIR_ADAPTIVE=1): the scalar fp32 adaptive kernel
+#ifndef ENS_NO_PAIR_ADAPTIVE
+#define ENS_NO_PAIR_ADAPTIVE 0
+#endif
+
 namespace ens {
 
 // Bulk save rows must start on 16-byte boundaries: u_out aligned and ld·sizeof(T)
@@ -65,6 +70,13 @@ ens_status run_tsit5(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
     // 4.31 -> 4.10 ms, fp32 C2 adaptive 4.09 -> 4.05 ms; profiles/ab_r02/)
     if constexpr (!HasEvent<M>::value) {
       if (!opt->refill) {
+        if constexpr (std::is_same<T, float>::value && M::n >= 2 && !ENS_NO_PAIR_ADAPTIVE) {
+          // fp32: component pairs on the packed FFMA2 path (bit-identical to the scalar kernel)
+          auto kern = save ? tsit5_static_pair_kernel<M, true> : tsit5_static_pair_kernel<M, false>;
+          const dim3 b(occupancy_block(kern, a.N));
+          kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
+          return launch_status();
+        }
         auto kern = save ? tsit5_static_kernel<M, T, true> : tsit5_static_kernel<M, T, false>;
         const dim3 b(occupancy_block(kern, a.N));
         kern<<<dim3((unsigned)cdiv(a.N, b.x)), b, 0, s>>>(a);
