@@ -45,7 +45,7 @@ typedef enum {
   ENS_E_BAD_TOLERANCE = 4,        /* adaptive with abstol <= 0 or reltol < 0 or non-finite */
   ENS_E_BAD_TSPAN = 5,            /* t0 >= tf, dt <= 0, or a non-finite value */
   ENS_E_BAD_SAVEAT = 6,           /* saveat not strictly increasing, outside [t0,tf], or off the step grid
-                                     (EM / SIEA / fixed-step Vern7, Vern9 and Rodas5) */
+                                     (EM / SIEA) */
   ENS_E_WORKSPACE = 7,            /* workspace NULL or smaller than ens_workspace_bytes() */
   ENS_E_UNSUPPORTED = 8,          /* valid but not built (e.g. Rosenbrock23 on an SDE model's drift) */
   ENS_E_CUDA = 9                  /* a CUDA runtime call or kernel launch failed */
@@ -82,11 +82,13 @@ typedef enum {
   ENS_SIEA = 3,            /* weak order 2.0 stochastic improved Euler, fixed step, diagonal noise (R19) */
   ENS_RODAS4 = 4,          /* 4th-order stiffly accurate Rosenbrock, L-stable, fixed or adaptive (R20);
                               ODE models without events; POLLU fp64 only */
-  ENS_VERN7 = 5,           /* Verner 7(6), fixed or adaptive (R21); saves keep full order: fixed
-                              step — saveat on the step grid; adaptive — steps clipped to land on saveat.
+  ENS_VERN7 = 5,           /* Verner 7(6), fixed or adaptive (R21); dense output (R24): a save point
+                              τ inside a step [t, t+h] stores one Verner step from t of length τ − t (full
+                              order; the step sequence does not depend on saveat; any τ in [t0, tf]).
                               ODE models with n <= 8 and no events */
   ENS_RODAS5 = 6,          /* Rodas5 (Di Marzo), 5th-order stiffly accurate Rosenbrock, L-stable (R22:
-                              the method Rodas5P re-optimises); saves as ENS_VERN7; POLLU fp64 only */
+                              the method Rodas5P re-optimises); dense output as ENS_VERN7 (one Rodas5
+                              step of length τ − t; NaN if its W is singular); POLLU fp64 only */
   ENS_VERN9 = 7,           /* Verner 9(8), 16 stages, fixed or adaptive (R21); saves and models as
                               ENS_VERN7 */
   ENS_RODAS5P = 8          /* Rodas5P (Steinebach's re-optimised Rodas5; GPURodas5P, Table 4's

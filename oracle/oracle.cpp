@@ -1138,7 +1138,7 @@ static void solve_rodas4(const Opts& o, Traj<T>& tr) {
 // Rodas5P (below, R23) re-optimises. Same W-form and conventions as Rodas4: Y7 = Y6 + k6, Y8 = Y7 + k7,
 // u_new = Y8 + k8, E = k8. Pinned by the Rosenbrock B-series order conditions
 // (every rooted tree of order ≤ 5; tests/test_oracle_rodas5.py). No dense
-// output is recoverable either: saves clip the step like Vern7 (R21).
+// output is recoverable either: saves use the shortened-step dense output (R24).
 static const double RD5_GAMMA = 0.19;
 static const double RD5_A[8][7] = {
   {0, 0, 0, 0, 0, 0, 0},
@@ -1167,8 +1167,8 @@ static const Ctrl CTRL_RODAS5 = {7.0 / 50.0, 2.0 / 25.0, 0.9, 5.0, 0.1, 1e-4};  
 // (Y7 = Y6 + k6, Y8 = Y7 + k7, E = k8), γ = 0.21193756319429014. Coefficients
 // as published; pinned by the Rosenbrock B-series conditions of every rooted tree
 // of order ≤ 5 (main) / ≤ 4 (embedded) to 2e-14 with order 6 violated
-// (tests/test_oracle_rodas5p.py) — a mistyped digit fails them. Saves clip the
-// step like Rodas5 (R22).
+// (tests/test_oracle_rodas5p.py) — a mistyped digit fails them. Saves as Rodas5
+// (R24).
 static const double RD5P_GAMMA = 0.21193756319429014;
 static const double RD5P_A[8][7] = {
   {0, 0, 0, 0, 0, 0, 0},
@@ -1192,7 +1192,7 @@ static const double RD5P_C[8][7] = {
   {37.80277123390563, -3.2571969029072276, 112.26918849496327, 66.9347231244047, -40.06618937091002,
    -54.66780262877968, -9.48861652309627}};
 
-// The 8-stage clipping Rosenbrock tableaus (Rodas5, Rodas5P).
+// The 8-stage Rosenbrock tableaus without dense output (Rodas5, Rodas5P).
 struct Rd8Tab { double gamma; const double (*A)[7]; const double (*C)[7]; const Ctrl* ctrl; };
 static const Rd8Tab RODAS5_TAB = {RD5_GAMMA, RD5_A, RD5_C, &CTRL_RODAS5};
 static const Rd8Tab RODAS5P_TAB = {RD5P_GAMMA, RD5P_A, RD5P_C, &CTRL_RODAS5};   // p = 5 as well
@@ -1230,6 +1230,25 @@ static bool rodas5_step(const Rd8Tab& tb, int model, int n, const T* p, T t, T h
   return true;
 }
 
+// Dense output (DESIGN R24, as verner_saves): a save point τ ∈ (t, tn) stores one
+// Rodas step from (t, u) of length τ − t (its own J, W = I − (τ − t)γJ and LU);
+// if that W is singular the saved value is NaN. τ = tn stores u_new.
+template <class T>
+static void rodas5_saves(const Rd8Tab& tb, int model, int n, const T* p, T t, T tn, const T* u, const T* F0,
+                         const T* unew, const T* tau, int k, int* js, T* save) {
+  while (*js < k && tau[*js] <= tn) {
+    if (tau[*js] == tn) {
+      put(save, n, *js, unew);
+    } else {
+      T o[NMAX], E[NMAX];
+      if (!rodas5_step<T>(tb, model, n, p, t, tau[*js] - t, u, F0, o, E))
+        for (int c = 0; c < n; ++c) o[c] = std::numeric_limits<T>::quiet_NaN();
+      put(save, n, *js, o);
+    }
+    ++*js;
+  }
+}
+
 template <class T>
 static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const int n = tr.n, model = o.model;
@@ -1245,8 +1264,7 @@ static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int
   T t = (T)o.t0;
   const T tf = (T)o.tf, abstol = (T)o.abstol, reltol = (T)o.reltol;
   rhs<T>(model, u, p, t, F0);
-  if (!o.adaptive) { while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; } }
-  else { while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; } }
+  while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; }   // τ_j ≤ t0 (DESIGN R5)
   if (!finite_vec(F0, n)) tr.retcode = RET_DIVERGED;
   else if (!o.adaptive) {
     int64_t nsteps; double h_last;
@@ -1257,10 +1275,11 @@ static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int
       const T h = last ? hl : hdt;
       t = (T)(o.t0 + (double)i * o.dt);
       if (!rodas5_step<T>(tb, model, n, p, t, h, u, F0, unew, E)) { tr.retcode = RET_SINGULAR; break; }
+      const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
+      rodas5_saves<T>(tb, model, n, p, t, tn, u, F0, unew, tau.data(), k, &js, tr.save);
       for (int j = 0; j < n; ++j) u[j] = unew[j];
-      if (!last) rhs<T>(model, u, p, (T)(o.t0 + (double)(i + 1) * o.dt), F0);
+      if (!last) rhs<T>(model, u, p, tn, F0);
       tr.n_accept++;
-      while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
     }
     t = tf;
     if (tr.retcode == RET_SUCCESS && !finite_vec(u, n)) tr.retcode = RET_DIVERGED;
@@ -1270,9 +1289,8 @@ static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
-      const T target = (js < k) ? tau[js] : tf;                   // next save point (or tf), R21 rule
-      const bool clip = (t + h >= target);
-      if (clip) h = target - t;
+      const bool last = (t + h >= tf);
+      if (last) h = tf - t;
       ++attempts;
       if (!rodas5_step<T>(tb, model, n, p, t, h, u, F0, unew, E)) {
         h = h * T(0.5);                                   // singular W: reject, halve (DESIGN R10)
@@ -1282,9 +1300,10 @@ static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int
       }
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       if (accept_q<T>(q2)) {
-        t = clip ? target : t + h;
+        const T tn = last ? tf : t + h;
+        rodas5_saves<T>(tb, model, n, p, t, tn, u, F0, unew, tau.data(), k, &js, tr.save);
+        t = tn;
         for (int j = 0; j < n; ++j) u[j] = unew[j];
-        if (clip && js < k) { put(tr.save, n, js, u); ++js; }
         rhs<T>(model, u, p, t, F0);
         tr.n_accept++;
         h = pi_accept<T>(C, h, q2, &lq_old);
@@ -1311,10 +1330,10 @@ static void solve_rodas5(const Rd8Tab& tb, const Opts& o, Traj<T>& tr, const int
 // tests/test_oracle_vern9.py); the embedded weights are the one direction the
 // order conditions leave, scaled by the published b̂1
 // (tools/derive_verner_embedded.py); stored as b̃ = b − b̂. Not FSAL: k1 = f(u)
-// is evaluated after each accepted step. Saves: fixed step — grid points only
-// (R11 rule); adaptive — the step is clipped to land on the next save point
-// (R21; the paper's lazy interpolants are not reproduced), so every saved value
-// carries the method's full order.
+// is evaluated after each accepted step. Saves: a save point inside a step
+// stores one step of the method from the step's start (verner_saves, R24; the
+// paper's lazy interpolants are not reproduced), so every saved value carries
+// the method's full order.
 static const double V7_C[10] = {0.0, 0.005, 0.10888888888888888, 0.16333333333333333, 0.4555,
                                 0.6095094489978381, 0.884, 0.925, 1.0, 1.0};
 static const double V7_A[10][9] = {
@@ -1420,6 +1439,28 @@ static void verner_step(const VernTab& tb, int model, int n, const T* p, T t, T 
   }
 }
 
+// Dense output (DESIGN R24, replacing round 2's step clipping): a save point
+// τ ∈ (t, tn) of an accepted step [t, tn] stores one step of the same method
+// from (t, u) of length τ − t — the method's own order at every saved value,
+// and the step sequence does not depend on saveat (the paper's lazy
+// interpolants, are likewise evaluated only for steps that contain a
+// save point). τ = tn stores u_new. F0 = f(u).
+template <class T>
+static void verner_saves(const VernTab& tb, int model, int n, const T* p, T t, T tn, const T* u, const T* F0,
+                         const T* unew, const T* tau, int k, int* js, T* save) {
+  while (*js < k && tau[*js] <= tn) {
+    if (tau[*js] == tn) {
+      put(save, n, *js, unew);
+    } else {
+      T K[16][NMAX], o[NMAX];
+      for (int c = 0; c < n; ++c) K[0][c] = F0[c];
+      verner_step<T>(tb, model, n, p, t, tau[*js] - t, u, K, o, nullptr);
+      put(save, n, *js, o);
+    }
+    ++*js;
+  }
+}
+
 template <class T>
 static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const int64_t* save_step) {
   const int n = tr.n, model = o.model;
@@ -1434,9 +1475,8 @@ static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const in
   T t = (T)o.t0;
   const T tf = (T)o.tf;
   rhs<T>(model, u, p, t, K[0]);
-  // saves at t0 (DESIGN R5): fixed step — grid index 0; adaptive — τ ≤ t0
-  if (!o.adaptive) { while (js < k && save_step[js] == 0) { put(tr.save, n, js, u); ++js; } }
-  else { while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; } }
+  // saves at τ_j ≤ t0 (DESIGN R5)
+  while (js < k && tau[js] <= t) { put(tr.save, n, js, u); ++js; }
   if (!finite_vec(K[0], n)) {
     tr.retcode = RET_DIVERGED;
   } else if (!o.adaptive) {
@@ -1448,11 +1488,11 @@ static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const in
       const T h = last ? hl : hdt;
       t = (T)(o.t0 + (double)i * o.dt);
       verner_step<T>(tb, model, n, p, t, h, u, K, unew, nullptr);
-      for (int j = 0; j < n; ++j) u[j] = unew[j];
       const T tn = last ? tf : (T)(o.t0 + (double)(i + 1) * o.dt);
+      verner_saves<T>(tb, model, n, p, t, tn, u, K[0], unew, tau.data(), k, &js, tr.save);
+      for (int j = 0; j < n; ++j) u[j] = unew[j];
       if (!last) rhs<T>(model, u, p, tn, K[0]);
       tr.n_accept++;
-      while (js < k && save_step[js] == i + 1) { put(tr.save, n, js, u); ++js; }
     }
     t = tf;
     if (!finite_vec(u, n)) tr.retcode = RET_DIVERGED;
@@ -1464,16 +1504,16 @@ static void solve_verner(const VernTab& tb, const Opts& o, Traj<T>& tr, const in
     int64_t attempts = 0;
     while (t < tf) {
       if (attempts >= o.max_steps) { tr.retcode = RET_MAXITERS; break; }
-      const T target = (js < k) ? tau[js] : tf;                   // next save point (or tf)
-      const bool clip = (t + h >= target);
-      if (clip) h = target - t;
+      const bool last = (t + h >= tf);
+      if (last) h = tf - t;
       verner_step<T>(tb, model, n, p, t, h, u, K, unew, E);
       const T q2 = error_q2<T>(n, E, u, unew, abstol, reltol);
       ++attempts;
       if (accept_q<T>(q2)) {
-        t = clip ? target : t + h;
+        const T tn = last ? tf : t + h;
+        verner_saves<T>(tb, model, n, p, t, tn, u, K[0], unew, tau.data(), k, &js, tr.save);
+        t = tn;
         for (int j = 0; j < n; ++j) u[j] = unew[j];
-        if (clip && js < k) { put(tr.save, n, js, u); ++js; }
         rhs<T>(model, u, p, t, K[0]);
         tr.n_accept++;
         h = pi_accept<T>(C, h, q2, &lq_old);
@@ -1596,8 +1636,7 @@ static int solve_all(const Opts& o, int64_t N, const T* u0, const T* p, int p_br
   const int n = d.n, m = d.m, k = o.k;
   // EM save points as step indices (DESIGN R11)
   std::vector<int64_t> save_step(k);
-  if (o.alg == EM || o.alg == SIEA ||
-      ((o.alg == VERN7 || o.alg == VERN9 || o.alg == RODAS5 || o.alg == RODAS5P) && !o.adaptive)) {
+  if (o.alg == EM || o.alg == SIEA) {
     // grid points are t0 + i·dt (i < nsteps) and tf itself (DESIGN R11)
     int64_t nsteps; double h_last;
     fixed_grid(o.t0, o.tf, o.dt, &nsteps, &h_last);

@@ -67,10 +67,13 @@ bool model_dims(int model, int* n, int* m, int* nw) {
 }
 
 inline bool is_sde_alg(int alg) { return alg == ENS_EM || alg == ENS_SIEA; }
-// save points given as step-grid indices (DESIGN R11; fixed-step Vern7 / Rodas5, R21-R22)
-inline bool grid_saves(int alg, const ens_options* opt) {
-  return is_sde_alg(alg) ||
-         ((alg == ENS_VERN7 || alg == ENS_VERN9 || alg == ENS_RODAS5 || alg == ENS_RODAS5P) && !opt->adaptive);
+// save points given as step-grid indices (DESIGN R11: EM / SIEA)
+inline bool grid_saves(int alg, const ens_options*) { return is_sde_alg(alg); }
+// fixed-step saves by save codes (fixed_save_codes): Tsit5 (interpolant) and the
+// dense-output-by-substep methods Vern7 / Vern9 / Rodas5 / Rodas5P (DESIGN R24)
+inline bool coded_saves(int alg, const ens_options* opt) {
+  return !opt->adaptive && (alg == ENS_TSIT5 || alg == ENS_VERN7 || alg == ENS_VERN9 || alg == ENS_RODAS5 ||
+                            alg == ENS_RODAS5P);
 }
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -237,8 +240,8 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
   a.chunk_stride = opt->chunk_stride;
   a.partial = (double*)(ws + L.partial);
   a.counter = (unsigned long long*)(ws + L.counter);
-  std::vector<int64_t> tsit_codes;   // fixed-step Tsit5 save codes (every chunk needs save_grid_only)
-  if (alg == ENS_TSIT5 && !opt->adaptive && a.k > 0) {
+  std::vector<int64_t> tsit_codes;   // fixed-step save codes (Tsit5: every chunk needs save_grid_only)
+  if (coded_saves(alg, opt) && a.k > 0) {
     std::vector<T> tau(a.k);
     for (int j = 0; j < a.k; ++j) tau[j] = (T)opt->saveat[j];
     fixed_save_codes<T>(t0, tf, dt, nsteps, tau, tsit_codes);
@@ -255,7 +258,7 @@ ens_status solve_impl(int model, int alg, int64_t N, int64_t ld, const void* u0,
         if (!em_save_steps(t0, tf, dt, opt->saveat, a.k, st)) return ENS_E_BAD_SAVEAT;
         if (cudaMemcpyAsync(ws + L.save_step, st.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return ENS_E_CUDA;
-      } else if (alg == ENS_TSIT5 && !opt->adaptive) {
+      } else if (coded_saves(alg, opt)) {
         if (cudaMemcpyAsync(ws + L.save_step, tsit_codes.data(), 8 * a.k, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return ENS_E_CUDA;
       }

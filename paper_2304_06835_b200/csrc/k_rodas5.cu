@@ -1,5 +1,5 @@
 // k_rodas5.cu — Rodas5 kernel instances (R22; fixed step with grid saves;
-// adaptive static or refill with step-clipped saves) for the ODE models without events.
+// adaptive static or refill; dense output by shortened steps, DESIGN R24) for the ODE models without events.
 #include <type_traits>
 
 #include "rodas5_launch.cuh"

@@ -1,5 +1,5 @@
 // k_rodas5p.cu — Rodas5P kernel instances (R23; fixed step with grid saves;
-// adaptive static or refill with step-clipped saves) for the ODE models without events.
+// adaptive static or refill; dense output by shortened steps, DESIGN R24) for the ODE models without events.
 #include <type_traits>
 
 #include "rodas5_launch.cuh"

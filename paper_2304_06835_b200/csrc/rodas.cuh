@@ -7,8 +7,9 @@
 // (S = 6 / 8); stiffly accurate, so the error estimate is the last stage k_S.
 // Like Rosenbrock23 there is no Newton iteration. All stage
 // vectors, J, W and its LU stay in registers for n ≤ 8. Rodas4 saves through
-// its dense output; Rodas5 (no recoverable dense output) clips steps onto save
-// points (R21 rule).
+// its dense output; Rodas5 / Rodas5P (their dense-output coefficients are not
+// recoverable offline) store at a save point one step of the method from the
+// step's start (R24), so the step sequence does not depend on saveat.
 #pragma once
 #include "common.cuh"
 #include "models_stiff.cuh"
@@ -317,9 +318,34 @@ __global__ void __launch_bounds__(256) rodas4_fixed_kernel(const Args<T> a) {
   if (a.nrej) a.nrej[i] = 0;
 }
 
-// Rodas5 (R22): adaptive lane whose saves clip the step onto the next save
-// point (R21 rule), and a fixed-step kernel saving on grid indices.
-template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
+// Dense output of Rodas5 / Rodas5P (DESIGN R24): every save point τ ∈ (t, tn] of
+// an accepted step [t, tn] — τ = tn stores u_new, an interior τ one step of the
+// method from (t, u) of length τ − t (its own W = I − (τ − t)γJ and LU; NaN if
+// that W is singular). Only steps containing a save point pay for it.
+template <class Tab, class M, class T>
+__device__ __forceinline__ void rodas_saves(const Args<T>& a, int64_t i, int& js, T t, T tn, const T (&par)[M::m],
+                                            const T (&u)[M::n], const T (&F0)[M::n], const T (&un)[M::n]) {
+  constexpr int n = M::n;
+  while (js < a.k) {
+    const T tau = __ldg(a.tau + js);
+    if (!(tau <= tn)) break;
+    if (tau == tn) {
+      store_point<n>(a, i, js, un);
+    } else {
+      T o[n], K[Tab::S][n];
+      if (!rodas_step<Tab, M, T>(par, t, tau - t, u, F0, o, K)) {
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+        for (int j = 0; j < n; ++j) o[j] = nanT<T>();
+      }
+      store_point<n>(a, i, js, o);
+    }
+    ++js;
+  }
+}
+
+// Rodas5 / Rodas5P (R22, R23): adaptive lane with the R24 dense output, and a
+// fixed-step kernel saving by the fixed-step save codes.
+template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;
@@ -340,9 +366,8 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
 
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
     if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
-    const T target = (SAVE && js < a.k) ? __ldg(a.tau + js) : a.tf;
-    const bool clip = (t + h >= target);
-    if (clip) h = target - t;
+    const bool last = (t + h >= a.tf);
+    if (last) h = a.tf - t;
     T un[n], K[Tab::S][n];
     if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) {
       h = h * T(0.5);                       // singular W: reject and halve (DESIGN R10)
@@ -352,10 +377,11 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
     }
     const T q2 = error_q2<n, T>(K[Tab::S - 1], u, un, a.abstol, a.reltol);
     if (q2 < T(1)) {
-      t = clip ? target : t + h;
+      const T tn = last ? a.tf : t + h;
+      if (SAVE) rodas_saves<Tab, M, T>(a, i, js, t, tn, par, u, F0, un);
+      t = tn;
 #pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
-      if (SAVE && clip && js < a.k) { store_point<n>(a, i, js, u); ++js; }
       M::f(u, par, t, F0);
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
@@ -383,7 +409,7 @@ template <class Tab, class M, class T, bool SAVE> struct RodasClipLane {
 };
 
 template <class Tab, class M, class T, bool SAVE>
-__global__ void __launch_bounds__(256) rodas_grid_fixed_kernel(const Args<T> a) {
+__global__ void __launch_bounds__(256) rodas_coded_fixed_kernel(const Args<T> a) {
   constexpr int n = M::n;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
@@ -403,13 +429,27 @@ __global__ void __launch_bounds__(256) rodas_grid_fixed_kernel(const Args<T> a) 
       const T t = (T)(a.t0d + (double)s * a.dtd);
       T un[n], K[Tab::S][n];
       if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) { ret = RET_SINGULAR; break; }
+      if (SAVE) {   // fixed-step save codes (verner_fixed_kernel); interp = the R24 dense output
+        while (js < a.k) {
+          const int64_t code = __ldg(a.save_step + js);
+          if ((code >> 1) != s + 1) break;
+          if (code & 1) {
+            T o[n];
+            if (!rodas_step<Tab, M, T>(par, t, __ldg(a.tau + js) - t, u, F0, o, K)) {
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+              for (int j = 0; j < n; ++j) o[j] = nanT<T>();
+            }
+            store_point<n>(a, i, js, o);
+          } else {
+            store_point<n>(a, i, js, un);
+          }
+          ++js;
+        }
+      }
 #pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];
       if (!last) M::f(u, par, (T)(a.t0d + (double)(s + 1) * a.dtd), F0);
       ++nacc;
-      if (SAVE) {
-        while (js < a.k && __ldg(a.save_step + js) == s + 1) { store_point<n>(a, i, js, u); ++js; }
-      }
     }
     if (ret == RET_SUCCESS && !all_finite<n>(u)) ret = RET_DIVERGED;
   }

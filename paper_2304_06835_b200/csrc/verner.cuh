@@ -5,8 +5,10 @@
 // Verner's pairs; the embedded weights are derived from the order conditions
 // (R21). All stage vectors stay in registers;
 // zero tableau entries are compile-time constants, so their terms vanish from
-// the instruction stream. Saves keep the full order (R21): fixed step — on
-// grid points; adaptive — the step is clipped to land on the next save point.
+// the instruction stream. Dense output (R24): a save point inside an accepted
+// step stores one step of the same method from the step's start to the save
+// point, so every saved value carries the method's order and the step
+// sequence does not depend on saveat.
 #pragma once
 #include "common.cuh"
 #include "models.cuh"
@@ -137,6 +139,29 @@ __device__ __forceinline__ void verner_step(const T (&par)[M::m], T t, T h, cons
   }
 }
 
+// Dense output (DESIGN R24): every save point τ ∈ (t, tn] of an accepted step
+// [t, tn] — τ = tn stores u_new, an interior τ one step of the method from
+// (t, u) of length τ − t (computed only for steps that contain a save point,
+// like the paper's lazy interpolants). K[0] = f(u) on entry; the
+// main step's other stage vectors are dead here and are reused.
+template <class Tab, class M, class T>
+__device__ __forceinline__ void verner_saves(const Args<T>& a, int64_t i, int& js, T t, T tn, const T (&par)[M::m],
+                                             const T (&u)[M::n], T (&K)[Tab::S][M::n], const T (&un)[M::n]) {
+  constexpr int n = M::n;
+  while (js < a.k) {
+    const T tau = __ldg(a.tau + js);
+    if (!(tau <= tn)) break;
+    if (tau == tn) {
+      store_point<n>(a, i, js, un);
+    } else {
+      T o[n], E[n];
+      verner_step<Tab, M, T, false>(par, t, tau - t, u, K, o, E);
+      store_point<n>(a, i, js, o);
+    }
+    ++js;
+  }
+}
+
 template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
@@ -158,19 +183,19 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
 
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
     if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
-    const T target = (SAVE && js < a.k) ? __ldg(a.tau + js) : a.tf;   // next save point or tf (R21)
-    const bool clip = (t + h >= target);
-    if (clip) h = target - t;
+    const bool last = (t + h >= a.tf);
+    if (last) h = a.tf - t;
     T K[Tab::S][n], un[n], E[n];
 #pragma unroll
     for (int c = 0; c < n; ++c) K[0][c] = F0[c];
     verner_step<Tab, M, T, true>(par, t, h, u, K, un, E);
     const T q2 = error_q2<n, T>(E, u, un, a.abstol, a.reltol);
     if (q2 < T(1)) {
-      t = clip ? target : t + h;
+      const T tn = last ? a.tf : t + h;
+      if (SAVE) verner_saves<Tab, M, T>(a, i, js, t, tn, par, u, K, un);
+      t = tn;
 #pragma unroll
       for (int c = 0; c < n; ++c) u[c] = un[c];
-      if (SAVE && clip && js < a.k) { store_point<n>(a, i, js, u); ++js; }
       M::f(u, par, t, F0);
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
@@ -197,7 +222,10 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   }
 };
 
-// Fixed-step Verner on the DESIGN R3 grid; saves at grid indices a.save_step.
+// Fixed-step Verner on the DESIGN R3 grid. Saves by the fixed-step save codes
+// of tsit5_save_coded (api.cu fixed_save_codes): code (s << 1) | interp is
+// stored during step s − 1 → s, u_s itself (interp = 0) or the dense output
+// of R24 from the step's start (interp = 1); code 0 = saved at t0.
 template <class Tab, class M, class T, bool SAVE>
 __global__ void __launch_bounds__(256) verner_fixed_kernel(const Args<T> a) {
   constexpr int n = M::n;
@@ -221,13 +249,24 @@ __global__ void __launch_bounds__(256) verner_fixed_kernel(const Args<T> a) {
 #pragma unroll
       for (int c = 0; c < n; ++c) K[0][c] = F0[c];
       verner_step<Tab, M, T, false>(par, t, h, u, K, un, E);
+      if (SAVE) {
+        while (js < a.k) {
+          const int64_t code = __ldg(a.save_step + js);
+          if ((code >> 1) != s + 1) break;
+          if (code & 1) {
+            T o[n];
+            verner_step<Tab, M, T, false>(par, t, __ldg(a.tau + js) - t, u, K, o, E);
+            store_point<n>(a, i, js, o);
+          } else {
+            store_point<n>(a, i, js, un);
+          }
+          ++js;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < n; ++c) u[c] = un[c];
       if (!last) M::f(u, par, (T)(a.t0d + (double)(s + 1) * a.dtd), F0);
       ++nacc;
-      if (SAVE) {
-        while (js < a.k && __ldg(a.save_step + js) == s + 1) { store_point<n>(a, i, js, u); ++js; }
-      }
     }
     if (!all_finite<n>(u)) ret = RET_DIVERGED;
   }

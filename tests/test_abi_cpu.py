@@ -87,12 +87,13 @@ def _call(model, alg, dtype=0, N=16, t0=0.0, tf=1.0, dt=1e-3, **o):
     (dict(model="pollu", alg="rodas4", dtype=0), 8),                               # POLLU: fp64 only
     (dict(model="lorenz", alg="rodas4", adaptive=1, abstol=-1.0), 4),
     (dict(model="lorenz", alg="rodas4"), 7),                                       # valid up to the workspace
-    (dict(model="lorenz", alg="vern7", saveat=[0.00015]), 6),                      # fixed Vern7: grid saves (R21)
+    (dict(model="lorenz", alg="vern7", saveat=[0.00015]), 7),                      # fixed Vern7: any τ (R24)
     (dict(model="lorenz", alg="vern7", adaptive=1, abstol=1e-8, saveat=[0.00015]), 7),   # adaptive: any τ
     (dict(model="gbm", alg="vern7"), 2),
-    (dict(model="lorenz", alg="rodas5", saveat=[0.00015]), 6),                     # fixed Rodas5: grid saves (R22)
+    (dict(model="lorenz", alg="rodas5", saveat=[0.00015]), 7),                     # fixed Rodas5: any τ (R24)
     (dict(model="ball", alg="rodas5", adaptive=1, abstol=1e-6), 8),
-    (dict(model="lorenz", alg="vern9", saveat=[0.00015]), 6),
+    (dict(model="lorenz", alg="vern9", saveat=[0.00015]), 7),
+    (dict(model="lorenz", alg="em", saveat=[0.00015]), 2),                          # EM: lorenz is an ODE model
     (dict(model="pollu", alg="vern9", dtype=1), 8),                                # n = 20: stiff solvers only
     (dict(model="lorenz", alg="tsit5", N=16, out_ld=8), 1),                        # out_ld < N
     (dict(model="lorenz", alg="tsit5", N=16, out_ld=32), 7),                       # wider rows: valid

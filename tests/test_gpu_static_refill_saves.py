@@ -33,7 +33,7 @@ def test_staged_saves_robertson(alg):
     assert a[1][5] == 3 and np.isnan(a[0][1:, :, 5]).all()
     # a cap that stops some lanes part-way: MaxIters with NaN-filled remaining rows
     a, b = _pair("robertson", alg, u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8, reltol=1e-8, saveat=sa,
-                 max_steps=200)
+                 max_steps=120)
     for x, y in zip(a[:4], b[:4]):
         np.testing.assert_array_equal(x, y)
     assert (a[1] == 1).any()

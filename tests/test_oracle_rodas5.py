@@ -2,7 +2,8 @@
 order conditions of every rooted tree up to order 5 (main) / 4 (embedded),
 L-stability and the stability function of one step, measured convergence
 orders, the Robertson / stiff-suite literature references (P:668-679,
-P:733-844) and the step-clipping save rule."""
+P:733-844) and the dense-output save rule (R24;
+tests/test_oracle_dense_output.py)."""
 import json
 import math
 from pathlib import Path
@@ -104,7 +105,7 @@ def test_rodas5_stiff_suite_references():
         assert na[0] < na4[0], (model, na[0], na4[0])
 
 
-def test_rodas5_saveat_clipping_and_controller():
+def test_rodas5_saveat_and_controller():
     sa = np.array([0.0, 0.37, 1.0, 2.2, 3.0])
     out, rc, *_ = oracle.solve("harmonic", "rodas5", [[1.0], [0.0]], [[1.0]], (0, 3.0), 0.1, adaptive=True,
                                abstol=1e-11, reltol=1e-11, saveat=sa)

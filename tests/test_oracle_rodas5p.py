@@ -4,7 +4,8 @@ tree up to order 5 (main) / 4 (embedded) — the published coefficients satisfy
 them to 2e-14 and violate order 6, so a mistyped digit fails — the stiffly
 accurate structure, L-stability and the stability function of one step,
 measured convergence orders, the Robertson / stiff-suite literature references
- and the step-clipping save rule."""
+(P:668-679, P:733-844) and the dense-output save rule (R24;
+tests/test_oracle_dense_output.py)."""
 import json
 import math
 from pathlib import Path
@@ -110,7 +111,7 @@ def test_rodas5p_stiff_suite_references():
         assert na[0] < 2 * na5[0], (model, na[0], na5[0])   # same order as Rodas5 (HIRES: 563 vs 415)
 
 
-def test_rodas5p_saveat_clipping_and_controller():
+def test_rodas5p_saveat_and_controller():
     sa = np.array([0.0, 0.37, 1.0, 2.2, 3.0])
     out, rc, *_ = oracle.solve("harmonic", "rodas5p", [[1.0], [0.0]], [[1.0]], (0, 3.0), 0.1, adaptive=True,
                                abstol=1e-11, reltol=1e-11, saveat=sa)

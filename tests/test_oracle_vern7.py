@@ -6,7 +6,8 @@ embedded b̂ = b − b̃), the embedded scale against the structural zeros
 b̂8 = b̂9 = 0 of Verner's 7(6) design (the order conditions leave one free
 scale; one zero fixes it and the other must then vanish too), against measured
 convergence orders on a closed-form and a nonlinear problem, and the saveat
-rule (step clipping) against plain runs to the same end time.
+rule against plain runs to the same end time (the dense output itself, R24:
+tests/test_oracle_dense_output.py).
 """
 import math
 
@@ -110,11 +111,10 @@ def test_vern7_adaptive_accuracy_and_efficiency():
     assert na[0] < nat[0] / 2, (na[0], nat[0])
 
 
-def test_vern7_saveat_clipping_rule():
-    """Adaptive saves land exactly on τ (the step is clipped, R21): the saved
-    value equals a run whose tspan ends at τ only while the step sequences
-    agree — here a single save at τ = tf, and for interior τ the values match
-    the closed form to the tolerance."""
+def test_vern7_saveat_rule():
+    """Adaptive saves (R24: interior τ by a shortened step from the step's
+    start): the saved values match the closed form to the tolerance, τ = t0
+    stores u0, and a single save at τ = tf equals the plain run's final state."""
     sa = np.array([0.0, 0.37, 1.0, 2.2, 3.0])
     out, rc, na, nr = oracle.solve("harmonic", "vern7", [[1.0], [0.0]], [[1.0]], (0, 3.0), 0.1, adaptive=True,
                                    abstol=1e-12, reltol=1e-12, saveat=sa)
