@@ -4,6 +4,8 @@
   python tools/ncu_summary.py full  gpurun_out/prof_X.ncu-rep  TAG  [N_traj FLOP_per_traj]
   python tools/ncu_summary.py metrics        (prints the --metrics list for the executed-FLOP counters)
   python tools/ncu_summary.py launches gpurun_out/launches_X.csv TAG
+  python tools/ncu_summary.py alias NAME=TAG [NAME=TAG ...]   (point the bench's side-measurement
+      entries, e.g. c2_adaptive_f32=exec_c2a_r02y, at a fresh capture in profiles/ncu_summary.json)
 
 full: key metrics of the captured kernel (time, DRAM bytes, pipe / issue
 utilisation, occupancy, registers) → profiles/ncu_full_TAG.json, and the
@@ -132,8 +134,20 @@ def launches(path: str, tag: str):
     print(json.dumps(res, indent=1))
 
 
+def alias(pairs):
+    summ = PROF / "ncu_summary.json"
+    s = json.loads(summ.read_text())
+    for pr in pairs:
+        name, tag = pr.split("=", 1)
+        s[name] = dict(s[tag])
+        print(name, "<-", tag, s[name].get("executed_flop_per_launch"))
+    summ.write_text(json.dumps(s, indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "metrics":
+    if sys.argv[1] == "alias":
+        alias(sys.argv[2:])
+    elif sys.argv[1] == "metrics":
         print(",".join(EXEC_METRICS))
     elif sys.argv[1] == "full":
         full(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None,
