@@ -30,6 +30,8 @@ for dt in [torch.float32, torch.float64]:
               bulk_saves=True)                                                                  # cp.async.bulk path
     ens.solve("lorenz", "tsit5", ub2, pb2, (0.0, 1.0), 1e-2, saveat=[0.0, 0.333, 1.0])      # interpolated
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
+    ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6,
+              saveat=[0.0, 0.123, 0.5, 1.0])                        # static (fp32: component-pair kernel) + saves
     ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True,
               saveat=sa)
     ur, pr = ens.generate_inputs("robertson", "random10", N, dtype=dt, seed=3)
@@ -40,15 +42,17 @@ for dt in [torch.float32, torch.float64]:
     # Lorenz W = I − h d J needs row exchanges in some warps: the LU fast path's vote + rebuild
     ens.solve("lorenz", "rosenbrock23", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
     ens.solve("lorenz", "rodas5", u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6)
-    for alg in ["rodas4", "rodas5"]:
+    for alg in ["rodas4", "rodas5", "rodas5p"]:
         ens.solve("robertson", alg, ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6,
                   saveat=np.linspace(0, 10, 4))
         ens.solve("robertson", alg, ur, pr, (0.0, 10.0), 1e-4, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True)
         ens.solve("robertson", alg, ur, pr, (0.0, 1.0), 0.01, saveat=[0.0, 0.5, 1.0])
+        ens.solve("robertson", alg, ur, pr, (0.0, 1.0), 0.01, saveat=[0.0, 0.257, 0.5, 0.9999])   # off-grid (R24)
     for alg in ["vern7", "vern9"]:
         ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, saveat=sa)
         ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, adaptive=True, abstol=1e-6, reltol=1e-6, refill=True)
         ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, saveat=[0.0, 0.5, 1.0])
+        ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-2, saveat=[0.0, 0.005, 0.5, 0.777, 1.0])   # off-grid (R24)
     us, ps = ens.generate_inputs("lorenz_sde_mul", "const", N, dtype=dt)
     ens.solve("lorenz_sde_mul", "em", us, ps, (0.0, 0.1), 1e-3, seed=5, saveat=np.linspace(0, 0.1, 3), stats=True,
               store_states=False)
