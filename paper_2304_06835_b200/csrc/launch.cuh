@@ -76,12 +76,6 @@ void launch_adaptive(const Args<T>& a, bool refill, cudaStream_t s) {
   }
 }
 
-// Group kernels (group.cuh): G lanes per trajectory, 256-thread blocks.
-template <class K, class T>
-void launch_group(K kern, int G, const Args<T>& a, cudaStream_t s) {
-  kern<<<dim3((unsigned)cdiv(a.N * G, 256)), dim3(256), 0, s>>>(a);
-}
-
 // One-thread-per-trajectory launch of a fixed-step kernel with the occupancy-tuned block.
 template <class K, class T>
 void launch_fixed(K kern, const Args<T>& a, cudaStream_t s) {

@@ -3,13 +3,7 @@
 // slowest units to compile, so they build in parallel with the rest).
 #pragma once
 #include "launch.cuh"
-#include "group.cuh"
 #include "rodas.cuh"
-
-// A/B builds only (tools/build_variant.py -DENS_NO_GROUP=1): the per-thread kernels for HIRES / POLLU
-#ifndef ENS_NO_GROUP
-#define ENS_NO_GROUP 0
-#endif
 
 namespace ens {
 
@@ -20,14 +14,6 @@ ens_status run_rodas4(const Args<T>& a, const ens_options* opt, cudaStream_t s) 
     if (save) launch_fixed(rodas4_fixed_kernel<M, T, true>, a, s);
     else launch_fixed(rodas4_fixed_kernel<M, T, false>, a, s);
   } else {
-    if constexpr (kUseGroup<M> && !ENS_NO_GROUP) {
-      if (!opt->refill) {   // HIRES / POLLU: one trajectory per group of lanes (group.cuh; bit-identical)
-        constexpr int G = kGroupWidth<M::n>;
-        if (save) launch_group(rodas_group_kernel<Rodas4Tab, M, T, G, true, 0>, G, a, s);
-        else launch_group(rodas_group_kernel<Rodas4Tab, M, T, G, false, 0>, G, a, s);
-        return launch_status();
-      }
-    }
     if (save) launch_adaptive<Rodas4Lane<M, T, true>, T>(a, opt->refill, s);
     else launch_adaptive<Rodas4Lane<M, T, false>, T>(a, opt->refill, s);
   }

@@ -4,27 +4,13 @@
 // build in parallel with the rest).
 #pragma once
 #include "launch.cuh"
-#include "group.cuh"
 #include "rodas.cuh"
-
-// A/B builds only (tools/build_variant.py -DENS_NO_GROUP=1): the per-thread kernels for HIRES / POLLU
-#ifndef ENS_NO_GROUP
-#define ENS_NO_GROUP 0
-#endif
 
 namespace ens {
 
 template <class Tab, class M, class T>
 ens_status run_rodas_sub(const Args<T>& a, const ens_options* opt, cudaStream_t s) {
   const bool save = a.k > 0;
-  if constexpr (kUseGroup<M> && !ENS_NO_GROUP) {
-    if (opt->adaptive && !opt->refill) {   // HIRES / POLLU: one trajectory per group of lanes (group.cuh)
-      constexpr int G = kGroupWidth<M::n>;
-      if (save) launch_group(rodas_group_kernel<Tab, M, T, G, true, 1>, G, a, s);
-      else launch_group(rodas_group_kernel<Tab, M, T, G, false, 1>, G, a, s);
-      return launch_status();
-    }
-  }
   if (!opt->adaptive) {
     if (save) launch_fixed(rodas_coded_fixed_kernel<Tab, M, T, true>, a, s);
     else launch_fixed(rodas_coded_fixed_kernel<Tab, M, T, false>, a, s);
