@@ -10,7 +10,7 @@ comparing the checksums). Configs: c3 (Robertson Rosenbrock23 fp64 1e-8, saveat
 100, N=10^6), c3r5 / c3r4 (the same on Rodas5 / Rodas4), c2a (Lorenz Tsit5 fp32 1e-6 ρ sweep,
 N=10^7), c1t (Lorenz Tsit5 fp64 1e-10 ρ sweep, N=10^6), t9 / t7 (the same on Vern9 / Vern7),
 c2f (Lorenz Tsit5 fixed fp32 10^7), dense / dense1 (the same with all 1001 grid points saved, N = 4·10^6 / 10^6), orego/hires/pollu (stiff suite, Rosenbrock23, 8192; suffix 4 / 5:
-Rodas4 / Rodas5)."""
+Rodas4 / Rodas5; suffix 5p: Rodas5P; AB_REFILL=1 in the environment: the refill scheduler)."""
 import json
 import subprocess
 import sys
@@ -49,12 +49,14 @@ elif cfg in ("dense", "dense1"):
 elif cfg == "c2f":
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", 10**7, dtype=F32, N_total=10**7)
     f = lambda: ens.solve("lorenz", "tsit5", u0, p, (0.0, 1.0), 1e-3, stats=True)
-elif cfg.rstrip("45") in ("orego", "hires", "pollu"):
-    mdl = cfg.rstrip("45")
-    alg = {"4": "rodas4", "5": "rodas5"}.get(cfg[-1], "rosenbrock23")
+elif cfg.rstrip("45p") in ("orego", "hires", "pollu"):
+    mdl = cfg.rstrip("45p")
+    alg = "rodas5p" if cfg.endswith("5p") else {"4": "rodas4", "5": "rodas5"}.get(cfg[-1], "rosenbrock23")
     tf = {"orego": 30.0, "hires": 321.8122, "pollu": 60.0}[mdl]
     u0, p = ens.generate_inputs(mdl, "random10", 8192, dtype=F64, seed=0x57)
-    f = lambda: ens.solve(mdl, alg, u0, p, (0.0, tf), 1e-6, adaptive=True, abstol=1e-8, reltol=1e-8)
+    import os
+    rf = os.environ.get("AB_REFILL", "0") == "1"
+    f = lambda: ens.solve(mdl, alg, u0, p, (0.0, tf), 1e-6, adaptive=True, abstol=1e-8, reltol=1e-8, refill=rf)
 sol = f(); torch.cuda.synchronize()
 best = 1e30
 for _ in range(5):
