@@ -318,44 +318,27 @@ __global__ void __launch_bounds__(256) rodas4_fixed_kernel(const Args<T> a) {
   if (a.nrej) a.nrej[i] = 0;
 }
 
-// Dense output of Rodas5 / Rodas5P (DESIGN R24): every save point τ ∈ (t, tn] of
-// an accepted step [t, tn] — τ = tn stores u_new, an interior τ one step of the
-// method from (t, u) of length τ − t (its own W = I − (τ − t)γJ and LU; NaN if
-// that W is singular). Only steps containing a save point pay for it.
-template <class Tab, class M, class T>
-__device__ __forceinline__ void rodas_saves(const Args<T>& a, int64_t i, int& js, T t, T tn, const T (&par)[M::m],
-                                            const T (&u)[M::n], const T (&F0)[M::n], const T (&un)[M::n]) {
-  constexpr int n = M::n;
-  while (js < a.k) {
-    const T tau = __ldg(a.tau + js);
-    if (!(tau <= tn)) break;
-    if (tau == tn) {
-      store_point<n>(a, i, js, un);
-    } else {
-      T o[n], K[Tab::S][n];
-      if (!rodas_step<Tab, M, T>(par, t, tau - t, u, F0, o, K)) {
-#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
-        for (int j = 0; j < n; ++j) o[j] = nanT<T>();
-      }
-      store_point<n>(a, i, js, o);
-    }
-    ++js;
-  }
-}
-
 // Rodas5 / Rodas5P (R22, R23): adaptive lane with the R24 dense output, and a
 // fixed-step kernel saving by the fixed-step save codes.
 template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
+  // Dense output (DESIGN R24): a save point τ inside an accepted step [t, tp]
+  // stores one Rodas step from (t, u) of length τ − t (its own W = I − (τ − t)γJ
+  // and LU; NaN if that W is singular). One call per attempted step or per such
+  // save point, through one rodas_step call site (a second inlined copy doubled
+  // the build time of the POLLU units); the same operations in the same order as
+  // storing the saves inside the accepting call.
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;
   int32_t nacc, nrej, ret, js;
   bool done;
+  T up[n], tp;      // SAVE: the accepted step's end state and time while its interior saves are produced
+  bool pend;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
     t = a.t0; h = a.dt0; lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false; pend = false;
     M::f(u, par, t, F0);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -364,33 +347,60 @@ template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
     else if (!(t < a.tf)) done = true;
   }
 
+  __device__ __forceinline__ void accept_end(const Args<T>& a, int64_t i) {
+    if (SAVE) {   // τ = tp stores u_new
+      while (js < a.k && __ldg(a.tau + js) <= tp) { store_point<n>(a, i, js, up); ++js; }
+    }
+    pend = false;
+    t = tp;
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+    for (int j = 0; j < n; ++j) u[j] = up[j];
+    M::f(u, par, t, F0);
+    if (!(t < a.tf)) done = true;
+    else if (t + h == t) { ret = RET_DTMIN; done = true; }
+  }
+
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
-    const bool last = (t + h >= a.tf);
-    if (last) h = a.tf - t;
-    T un[n], K[Tab::S][n];
-    if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) {
+    const bool sub = SAVE && pend;
+    bool last = false;
+    if (!sub) {
+      if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+      last = (t + h >= a.tf);
+      if (last) h = a.tf - t;
+    }
+    const T hs = sub ? __ldg(a.tau + js) - t : h;
+    T y[n], K[Tab::S][n];
+    const bool ok = rodas_step<Tab, M, T>(par, t, hs, u, F0, y, K);
+    if (sub) {
+      if (!ok) {
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+        for (int j = 0; j < n; ++j) y[j] = nanT<T>();
+      }
+      store_point<n>(a, i, js, y);
+      ++js;
+      if (!(js < a.k && __ldg(a.tau + js) < tp)) accept_end(a, i);
+      return;
+    }
+    if (!ok) {
       h = h * T(0.5);                       // singular W: reject and halve (DESIGN R10)
       ++nrej;
       if (t + h == t) { ret = RET_SINGULAR; done = true; }
       return;
     }
-    const T q2 = error_q2<n, T>(K[Tab::S - 1], u, un, a.abstol, a.reltol);
+    const T q2 = error_q2<n, T>(K[Tab::S - 1], u, y, a.abstol, a.reltol);
     if (q2 < T(1)) {
-      const T tn = last ? a.tf : t + h;
-      if (SAVE) rodas_saves<Tab, M, T>(a, i, js, t, tn, par, u, F0, un);
-      t = tn;
+      tp = last ? a.tf : t + h;
 #pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
-      for (int j = 0; j < n; ++j) u[j] = un[j];
-      M::f(u, par, t, F0);
+      for (int j = 0; j < n; ++j) up[j] = y[j];
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
+      if (SAVE && js < a.k && __ldg(a.tau + js) < tp) { pend = true; return; }
+      accept_end(a, i);
     } else {
       h = pi_reject<T>(h, q2, Tab::beta1);
       ++nrej;
+      if (t + h == t) { ret = RET_DTMIN; done = true; }   // t < tf here
     }
-    if (!(t < a.tf)) done = true;
-    else if (t + h == t) { ret = RET_DTMIN; done = true; }
   }
 
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
@@ -428,23 +438,29 @@ __global__ void __launch_bounds__(256) rodas_coded_fixed_kernel(const Args<T> a)
       const T h = last ? a.h_last : a.dt0;
       const T t = (T)(a.t0d + (double)s * a.dtd);
       T un[n], K[Tab::S][n];
-      if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) { ret = RET_SINGULAR; break; }
-      if (SAVE) {   // fixed-step save codes (verner_fixed_kernel); interp = the R24 dense output
-        while (js < a.k) {
+      // fixed-step save codes (verner_fixed_kernel): the step's interior save points first (R24
+      // steps of length τ − t from (t, u); NaN if that W is singular), then the step — one call site
+      bool ok;
+      const int js0 = js;
+      for (;;) {
+        bool sub = false;
+        T hs = h;
+        if (SAVE && js < a.k) {
           const int64_t code = __ldg(a.save_step + js);
-          if ((code >> 1) != s + 1) break;
-          if (code & 1) {
-            T o[n];
-            if (!rodas_step<Tab, M, T>(par, t, __ldg(a.tau + js) - t, u, F0, o, K)) {
-#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
-              for (int j = 0; j < n; ++j) o[j] = nanT<T>();
-            }
-            store_point<n>(a, i, js, o);
-          } else {
-            store_point<n>(a, i, js, un);
-          }
-          ++js;
+          if ((code >> 1) == s + 1 && (code & 1)) { sub = true; hs = __ldg(a.tau + js) - t; }
         }
+        ok = rodas_step<Tab, M, T>(par, t, hs, u, F0, un, K);
+        if (!sub) break;
+        if (!ok) {
+#pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
+          for (int j = 0; j < n; ++j) un[j] = nanT<T>();
+        }
+        store_point<n>(a, i, js, un);
+        ++js;
+      }
+      if (!ok) { js = js0; ret = RET_SINGULAR; break; }   // the step failed: its save points stay unreached (NaN)
+      if (SAVE) {   // τ = t_{s+1}
+        while (js < a.k && __ldg(a.save_step + js) == ((s + 1) << 1)) { store_point<n>(a, i, js, un); ++js; }
       }
 #pragma unroll (n <= kUnrollMax ? n : kPartialUnroll)
       for (int j = 0; j < n; ++j) u[j] = un[j];

@@ -139,40 +139,25 @@ __device__ __forceinline__ void verner_step(const T (&par)[M::m], T t, T h, cons
   }
 }
 
-// Dense output (DESIGN R24): every save point τ ∈ (t, tn] of an accepted step
-// [t, tn] — τ = tn stores u_new, an interior τ one step of the method from
-// (t, u) of length τ − t (computed only for steps that contain a save point,
-// like the paper's lazy interpolants). K[0] = f(u) on entry; the
-// main step's other stage vectors are dead here and are reused.
-template <class Tab, class M, class T>
-__device__ __forceinline__ void verner_saves(const Args<T>& a, int64_t i, int& js, T t, T tn, const T (&par)[M::m],
-                                             const T (&u)[M::n], T (&K)[Tab::S][M::n], const T (&un)[M::n]) {
-  constexpr int n = M::n;
-  while (js < a.k) {
-    const T tau = __ldg(a.tau + js);
-    if (!(tau <= tn)) break;
-    if (tau == tn) {
-      store_point<n>(a, i, js, un);
-    } else {
-      T o[n], E[n];
-      verner_step<Tab, M, T, false>(par, t, tau - t, u, K, o, E);
-      store_point<n>(a, i, js, o);
-    }
-    ++js;
-  }
-}
-
+// The lane: one attempted step per call. With saves, an accepted step whose
+// interval holds interior save points is completed over several calls — one
+// R24 dense-output step per call, through the same verner_step call site as the
+// attempts, so the stage code is inlined once (a second inlined copy doubled the
+// build time of these units). Same operations in the same order as storing the
+// saves inside the accepting call.
 template <class Tab, class M, class T, bool SAVE> struct VernerLane {
   static constexpr int n = M::n;
   T u[n], par[M::m], F0[n];
   T t, h, lq_old;   // lq_old = log2 q_old (DESIGN R2)
   int32_t nacc, nrej, ret, js;
   bool done;
+  T up[n], tp;      // SAVE: the accepted step's end state and time while its interior saves are produced
+  bool pend;
 
   __device__ __forceinline__ void init(const Args<T>& a, int64_t i) {
     load_column<M, T>(a, i, u, par);
     t = a.t0; h = a.dt0; lq_old = T(kLFloor);
-    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false;
+    nacc = nrej = 0; ret = RET_SUCCESS; js = 0; done = false; pend = false;
     M::f(u, par, t, F0);
     if (SAVE) {
       while (js < a.k && __ldg(a.tau + js) <= t) { store_point<n>(a, i, js, u); ++js; }
@@ -181,30 +166,53 @@ template <class Tab, class M, class T, bool SAVE> struct VernerLane {
     else if (!(t < a.tf)) done = true;
   }
 
+  // end of an accepted step [t, tp]: a save point at τ = tp stores u_new; advance
+  __device__ __forceinline__ void accept_end(const Args<T>& a, int64_t i) {
+    if (SAVE) {
+      while (js < a.k && __ldg(a.tau + js) <= tp) { store_point<n>(a, i, js, up); ++js; }
+    }
+    pend = false;
+    t = tp;
+#pragma unroll
+    for (int c = 0; c < n; ++c) u[c] = up[c];
+    M::f(u, par, t, F0);
+    if (!(t < a.tf)) done = true;
+    else if (t + h == t) { ret = RET_DTMIN; done = true; }
+  }
+
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
-    const bool last = (t + h >= a.tf);
-    if (last) h = a.tf - t;
-    T K[Tab::S][n], un[n], E[n];
+    const bool sub = SAVE && pend;   // an interior save point τ ∈ (t, tp) of the accepted step
+    bool last = false;
+    if (!sub) {
+      if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+      last = (t + h >= a.tf);
+      if (last) h = a.tf - t;
+    }
+    const T hs = sub ? __ldg(a.tau + js) - t : h;
+    T K[Tab::S][n], y[n], E[n];
 #pragma unroll
     for (int c = 0; c < n; ++c) K[0][c] = F0[c];
-    verner_step<Tab, M, T, true>(par, t, h, u, K, un, E);
-    const T q2 = error_q2<n, T>(E, u, un, a.abstol, a.reltol);
+    verner_step<Tab, M, T, true>(par, t, hs, u, K, y, E);
+    if (sub) {                        // R24: the step of length τ − t from (t, u)
+      store_point<n>(a, i, js, y);
+      ++js;
+      if (!(js < a.k && __ldg(a.tau + js) < tp)) accept_end(a, i);
+      return;
+    }
+    const T q2 = error_q2<n, T>(E, u, y, a.abstol, a.reltol);
     if (q2 < T(1)) {
-      const T tn = last ? a.tf : t + h;
-      if (SAVE) verner_saves<Tab, M, T>(a, i, js, t, tn, par, u, K, un);
-      t = tn;
+      tp = last ? a.tf : t + h;
 #pragma unroll
-      for (int c = 0; c < n; ++c) u[c] = un[c];
-      M::f(u, par, t, F0);
+      for (int c = 0; c < n; ++c) up[c] = y[c];
       ++nacc;
       h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
+      if (SAVE && js < a.k && __ldg(a.tau + js) < tp) { pend = true; return; }
+      accept_end(a, i);
     } else {
       h = pi_reject<T>(h, q2, Tab::beta1);
       ++nrej;
+      if (t + h == t) { ret = RET_DTMIN; done = true; }   // t < tf here
     }
-    if (!(t < a.tf)) done = true;
-    else if (t + h == t) { ret = RET_DTMIN; done = true; }
   }
 
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
@@ -246,22 +254,24 @@ __global__ void __launch_bounds__(256) verner_fixed_kernel(const Args<T> a) {
       const T h = last ? a.h_last : a.dt0;
       const T t = (T)(a.t0d + (double)s * a.dtd);
       T K[Tab::S][n], un[n], E[n];
-#pragma unroll
-      for (int c = 0; c < n; ++c) K[0][c] = F0[c];
-      verner_step<Tab, M, T, false>(par, t, h, u, K, un, E);
-      if (SAVE) {
-        while (js < a.k) {
+      // the step's interior save points first (R24 steps of length τ − t from (t, u)), then
+      // the step itself — one verner_step call site
+      for (;;) {
+        bool sub = false;
+        T hs = h;
+        if (SAVE && js < a.k) {
           const int64_t code = __ldg(a.save_step + js);
-          if ((code >> 1) != s + 1) break;
-          if (code & 1) {
-            T o[n];
-            verner_step<Tab, M, T, false>(par, t, __ldg(a.tau + js) - t, u, K, o, E);
-            store_point<n>(a, i, js, o);
-          } else {
-            store_point<n>(a, i, js, un);
-          }
-          ++js;
+          if ((code >> 1) == s + 1 && (code & 1)) { sub = true; hs = __ldg(a.tau + js) - t; }
         }
+#pragma unroll
+        for (int c = 0; c < n; ++c) K[0][c] = F0[c];
+        verner_step<Tab, M, T, false>(par, t, hs, u, K, un, E);
+        if (!sub) break;
+        store_point<n>(a, i, js, un);
+        ++js;
+      }
+      if (SAVE) {   // τ = t_{s+1}
+        while (js < a.k && __ldg(a.save_step + js) == ((s + 1) << 1)) { store_point<n>(a, i, js, un); ++js; }
       }
 #pragma unroll
       for (int c = 0; c < n; ++c) u[c] = un[c];

@@ -45,7 +45,7 @@ def test_c2_adaptive_full_size_sampled():
                    (_take(sol.n_accept, idx), _take(sol.n_reject, idx)), (ona, onr), tol=1e-4, tol_same=1e-5, ref=ref)
 
 
-@pytest.mark.parametrize("alg", ["rosenbrock23", "rodas5"])
+@pytest.mark.parametrize("alg", ["rosenbrock23", "rodas5", "rodas5p"])
 def test_c3_full_size_sampled(alg):
     """C3: Robertson ±10 % rates, fp64, N = 10^6, tol 1e-8, h0 = 1e-4, 100 save
     points over [0, 1e5] (2.4 GB of states)."""
