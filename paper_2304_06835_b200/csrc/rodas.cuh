@@ -360,7 +360,14 @@ template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
     else if (t + h == t) { ret = RET_DTMIN; done = true; }
   }
 
+  // n ≤ 4: the dense-output steps inside the accepting call (a second inlined copy of the
+  // stage code; 4 % faster on C3, profiles/ab_r02/ab_r24_sites_r02z3.jsonl — cheap to build)
+  static constexpr bool kInlineSaves = (n <= 4);
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
+    if constexpr (kInlineSaves) {
+      step_inline(a, i);
+      return;
+    }
     const bool sub = SAVE && pend;
     bool last = false;
     if (!sub) {
@@ -401,6 +408,51 @@ template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
       ++nrej;
       if (t + h == t) { ret = RET_DTMIN; done = true; }   // t < tf here
     }
+  }
+
+  __device__ __forceinline__ void step_inline(const Args<T>& a, int64_t i) {
+    if (nacc + nrej >= a.max_steps) { ret = RET_MAXITERS; done = true; return; }
+    const bool last = (t + h >= a.tf);
+    if (last) h = a.tf - t;
+    T un[n], K[Tab::S][n];
+    if (!rodas_step<Tab, M, T>(par, t, h, u, F0, un, K)) {
+      h = h * T(0.5);                       // singular W: reject and halve (DESIGN R10)
+      ++nrej;
+      if (t + h == t) { ret = RET_SINGULAR; done = true; }
+      return;
+    }
+    const T q2 = error_q2<n, T>(K[Tab::S - 1], u, un, a.abstol, a.reltol);
+    if (q2 < T(1)) {
+      const T tn = last ? a.tf : t + h;
+      if (SAVE) {
+        while (js < a.k) {
+          const T tau = __ldg(a.tau + js);
+          if (!(tau <= tn)) break;
+          if (tau == tn) {
+            store_point<n>(a, i, js, un);
+          } else {
+            T o[n];
+            if (!rodas_step<Tab, M, T>(par, t, tau - t, u, F0, o, K)) {
+#pragma unroll
+              for (int j = 0; j < n; ++j) o[j] = nanT<T>();
+            }
+            store_point<n>(a, i, js, o);
+          }
+          ++js;
+        }
+      }
+      t = tn;
+#pragma unroll
+      for (int j = 0; j < n; ++j) u[j] = un[j];
+      M::f(u, par, t, F0);
+      ++nacc;
+      h = pi_accept<T>(h, q2, lq_old, Tab::beta1, Tab::beta2);
+    } else {
+      h = pi_reject<T>(h, q2, Tab::beta1);
+      ++nrej;
+    }
+    if (!(t < a.tf)) done = true;
+    else if (t + h == t) { ret = RET_DTMIN; done = true; }
   }
 
   __device__ __forceinline__ void finish(const Args<T>& a, int64_t i) {
