@@ -115,3 +115,16 @@ def test_rodas5_stiff_dense_output():
         y40 = np.array(ROB["t40"])   # Hairer–Wanner reference (tests/golden/robertson_reference.json)
         assert np.abs(out[3, :, 0] - y40).max() / np.abs(y40) .max() < 1e-6
         assert math.isfinite(out[1, 1, 0])
+
+
+@pytest.mark.parametrize("alg", list(ALGS))
+def test_tiny_and_end_offsets(alg):
+    """A save point a hair after a grid point (τ − t_s = 1e-13) stores a step of
+    that length — u_s to within 1e-12 — and one a hair before the next grid point
+    agrees with u_{s+1} to the local error of the method (fixed dt = 0.1)."""
+    taus = [0.5, 0.5 + 1e-13, 0.6 - 1e-13, 0.6]
+    out, rc, *_ = oracle.solve("harmonic", alg, HARM["u0"], HARM["p"], (0.0, 1.0), 0.1, saveat=taus)
+    assert rc[0] == 0
+    np.testing.assert_allclose(out[1, :, 0], out[0, :, 0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(out[2, :, 0], out[3, :, 0], rtol=0, atol=1e-11)
+    assert np.abs(out[:, :, 0] - _exact(taus)).max() < 1e-6
