@@ -471,7 +471,8 @@ def main():
                                                   f"frac_fp64_peak_{fl:.0f}flop_per_attempt":
                                                       att * fl / (mst / 1e3) / pk64,
                                                   "frac_fp64_peak_executed":
-                                                      executed_frac({"tsit5": "c1t_tsit5_f64_tol1e-10"}.get(alg, ""),
+                                                      executed_frac({"tsit5": "c1t_tsit5_f64_tol1e-10",
+                                                                    "vern9": "t9_vern9_f64_tol1e-10"}[alg],
                                                                     n_t, mst, pk64)}
         del u0t, pt, sol_t
         # NEXT-2: C3 (Robertson fp64, tol 1e-8, 100 save points) on Rosenbrock23 vs Rodas5

@@ -42,7 +42,8 @@ python tools/ncu_summary.py full $OUT/prof_tsit5_$TAG.ncu-rep tsit5_fixed_lorenz
   > /dev/null 2>&1 && cp profiles/ncu_full_tsit5_fixed_lorenz_f32_$TAG.json $OUT/
 # executed-FLOP counters of the side kernels: summarised here, the ~10 MB reports are not brought back
 for cs in c2f64:tsit5_fixed:10000000 c2a:static_pair_kernel:10000000 c1t:static_kernel:1000000 \
-          c3:static_kernel:1000000 c3r5:static_kernel:1000000 c3r5p:static_kernel:1000000; do
+          c3:static_kernel:1000000 c3r5:static_kernel:1000000 c3r5p:static_kernel:1000000 \
+          t9:static_kernel:1000000; do
   IFS=: read name kern n <<< "$cs"
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,$EXEC \
     --clock-control none -k regex:$kern -s 1 -c 1 -o $OUT/prof_exec_${name}_$TAG -f \

@@ -4,7 +4,7 @@ NAME: c2f32 / c2f64 (Lorenz tsit5 fixed, rho sweep, fused stats), c1t (Lorenz ts
 c2a (Lorenz tsit5 adaptive fp32 1e-6 rho sweep), c3 (Robertson ros23 fp64
 saveat 100), c3r5 (the same on Rodas5), c4 (stochastic Lorenz EM fp32 stats),
 c4d (the same fp64), c1 (Lorenz fp64 adaptive 1e-8), tight9 / tight7 (Lorenz fp64
-1e-10 on Vern9 / Vern7, refill)."""
+1e-10 on Vern9 / Vern7, refill), t9 / t7 (the same, static mapping)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -63,12 +63,13 @@ elif name in ("c3r5", "c3r5p"):
     alg = "rodas5" if name == "c3r5" else "rodas5p"
     f = lambda: ens.solve("robertson", alg, u0, p, (0.0, 1e5), 1e-4, adaptive=True, abstol=1e-8,
                           reltol=1e-8, saveat=sa)
-elif name in ("tight9", "tight7"):
+elif name in ("tight9", "tight7", "t9", "t7"):
     N = N or 10**6
     u0, p = ens.generate_inputs("lorenz", "rho_sweep", N, dtype=torch.float64, N_total=N)
-    alg = "vern9" if name == "tight9" else "vern7"
+    alg = "vern9" if name.endswith("9") else "vern7"
+    rf = name.startswith("tight")     # tight*: refill scheduler; t9 / t7: static, as bench.py's side measurement
     f = lambda: ens.solve("lorenz", alg, u0, p, (0.0, 1.0), 1e-3, adaptive=True, abstol=1e-10, reltol=1e-10,
-                          refill=True)
+                          refill=rf)
 elif name == "c4d":
     N = N or 10**6
     u0, p = ens.generate_inputs("lorenz_sde_add", "const", N, dtype=torch.float64)
