@@ -555,6 +555,13 @@ def main():
                          "peak_basis": f"{props.multi_processor_count} SMs x {lanes} FMA lanes x 2 x {SM_MAX_MHZ:.0f} MHz",
                          "kernel_share_of_step": k_max / (ms_max / args.steps)},
             "clocks": clk.summary(),
+            # north_star: the paper's Lorenz ensemble numbers with their stated hardware, context only
+            # (2^31 Lorenz solves over 8 V100 nodes; the ODE solve of ≈306 M trajectories on one
+            # V100 took ≈1.6 s; step count / precision not stated)
+            "paper_context": {"source": "PAPER.md:395 (§6.3)", "gpu": "V100 (per node, 7 computing)",
+                              "trajectories_per_gpu": 306e6, "solve_seconds": 1.6,
+                              "trajectories_per_s_per_gpu": 306e6 / 1.6,
+                              "note": "other GPU, step count and precision unstated: context, not a baseline"},
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
             "also": also,
