@@ -54,3 +54,26 @@ def test_dense_fixed_offgrid_parity(alg, dtype):
     np.testing.assert_array_equal(rc, orc)
     np.testing.assert_array_equal(na, ona)
     check_fixed(g, o, {"f32": 1e-5, "f64": 1e-12}[dtype])
+
+
+@pytest.mark.parametrize("alg", list(CASES))
+def test_dense_adaptive_f32(alg):
+    """fp32 adaptive runs with interior save points: parity at the fp32 bars
+    (tests/helpers.check_adaptive: identical step counts on ≥ 99.9 %, rounding-level
+    agreement where they match, re-routed trajectories as accurate as the
+    oracle's own against an fp64 reference) and saveat-independent GPU step counts."""
+    model, recipe, seed, tspan, dt0, _ = CASES[alg]
+    N = 1031
+    u0, p = make_inputs(model, recipe, N, seed=seed + 1, dtype="f32")
+    sa = np.sort(np.concatenate([[tspan[0], tspan[1]], tspan[0] + (tspan[1] - tspan[0]) *
+                                 np.array([0.013, 0.2, 0.37, 0.5, 0.81])]))
+    kw = dict(adaptive=True, abstol=1e-5, reltol=1e-5)
+    g, rc, na, nr, _ = gpu(model, alg, u0, p, tspan, dt0, saveat=sa, **kw)
+    o, orc, ona, onr = oracle.solve(model, alg, u0, p, tspan, dt0, dtype="f32", saveat=sa, **kw)
+    ref, *_ = oracle.solve(model, alg, u0.astype(np.float64), p.astype(np.float64), tspan, dt0, dtype="f64",
+                           saveat=sa, adaptive=True, abstol=1e-9, reltol=1e-9)
+    np.testing.assert_array_equal(rc, orc)
+    check_adaptive(g, o, (na, nr), (ona, onr), tol=1e-2, tol_same=1e-5, ref=ref)
+    _, _, naf, nrf, _ = gpu(model, alg, u0, p, tspan, dt0, **kw)
+    np.testing.assert_array_equal(na, naf)
+    np.testing.assert_array_equal(nr, nrf)
