@@ -364,10 +364,11 @@ template <class Tab, class M, class T, bool SAVE> struct RodasSubLane {
   // stage code; 4 % faster on C3, profiles/ab_r02/ab_r24_sites_r02z3.jsonl — cheap to build)
   static constexpr bool kInlineSaves = (n <= 4);
   __device__ __forceinline__ void step(const Args<T>& a, int64_t i) {
-    if constexpr (kInlineSaves) {
-      step_inline(a, i);
-      return;
-    }
+    if constexpr (kInlineSaves) step_inline(a, i);
+    else step_one_site(a, i);
+  }
+
+  __device__ __forceinline__ void step_one_site(const Args<T>& a, int64_t i) {
     const bool sub = SAVE && pend;
     bool last = false;
     if (!sub) {
